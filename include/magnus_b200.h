@@ -1,0 +1,108 @@
+/*
+ * magnus_b200 -- C-ABI of the B200-native MAGNUS SpGEMM (C = A.B, CSR in, CSR out).
+ *
+ * The reference (arxiv/paper_2501_07056, /root/reference/pkg) is a Python
+ * package with no FFI; its boundary is the Python function
+ *     spgemm_magnus(A, B, sys=None, thresholds=None, threads=1, force_fine_only=False)
+ * (magnus.py:545-583) and its two phases magnus_symbolic (magnus.py:420-456)
+ * and magnus_numeric (magnus.py:459-542).  This header is what that function
+ * binds to (paper_2501_07056_b200/_lib.py, via ctypes): plain pointers and
+ * sizes, no torch types.  All array pointers are DEVICE pointers owned by the
+ * caller; the library only allocates its own workspace inside a magnus_ctx.
+ *
+ * Error convention (reference errors.py:4-27): every entry point returns a
+ * status code; magnus_last_error() returns the thread-local message.
+ */
+#ifndef MAGNUS_B200_H
+#define MAGNUS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MAGNUS_OK = 0,
+  MAGNUS_INPUT = 1,       /* InputError         errors.py:8    */
+  MAGNUS_CONTRACT = 2,    /* ContractViolation  errors.py:22   */
+  MAGNUS_OVER_BUDGET = 3, /* OverBudgetError    errors.py:26   */
+  MAGNUS_CUDA = 4         /* CUDA runtime error (no reference counterpart) */
+};
+
+enum { MAGNUS_CAT_SORT = 0, MAGNUS_CAT_DENSE = 1, MAGNUS_CAT_FINE = 2, MAGNUS_CAT_COARSE = 3 };
+
+/* CsrMatrix matrix.py:18-44.  row_ptr is int32 (rp_bytes=4) or int64 (8);
+ * col holds the reference's uint32 column indices (util.py:47-49). */
+typedef struct {
+  int64_t n_rows, n_cols, nnz;
+  const void* row_ptr;
+  int32_t rp_bytes;
+  const uint32_t* col;
+  const double* val;
+} magnus_csr;
+
+/* SystemParams planner.py:47-68 */
+typedef struct {
+  int64_t cache_line_bytes, l2_bytes, memory_budget_bytes, histo_type_bytes, prefix_sum_type_bytes, val_bytes;
+} magnus_sys;
+
+/* AccumThresholds accumulators.py:34-41 */
+typedef struct {
+  int64_t sort_dense_crossover, sort_sweet_spot;
+} magnus_thresholds;
+
+/* ChunkPlan planner.py:79-92 */
+typedef struct {
+  int64_t plan_cols, s_dense_accum, s_chunk_fine, n_chunks_fine, chunk_len_fine, shift_fine, m_max_l2, use_coarse,
+      n_chunks_coarse, chunk_len_coarse, shift_coarse;
+} magnus_chunk_plan;
+
+/* SpgemmResult.counters magnus.py:536-541 */
+typedef struct {
+  int64_t nnz_c, inter_prod_size, coarse_batches, rows_sort, rows_dense, rows_fine, rows_coarse;
+} magnus_counters;
+
+typedef struct magnus_ctx magnus_ctx;
+
+/* compute_chunk_plan planner.py:106-152 (host arithmetic, no device needed). */
+int magnus_compute_chunk_plan(const magnus_sys* sys, int64_t m_c, int numeric, int allow_coarse, magnus_chunk_plan* out);
+
+/* Context: owns the device workspace between the phases; bound to the current device. */
+int magnus_ctx_create(magnus_ctx** out);
+void magnus_ctx_destroy(magnus_ctx* ctx);
+
+/* Setup phase of spgemm_magnus (magnus.py:567-571): row_intermediate_stats
+ * (gustavson.py:97-134), both chunk plans, categorize_rows (magnus.py:68-94),
+ * build_coarse_batches' budget check (magnus.py:296-300).  A and B must stay
+ * alive and unmodified until magnus_numeric returns.  stream = cudaStream_t. */
+int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, const magnus_sys* sys,
+                 const magnus_thresholds* thresholds, int force_fine_only, void* stream);
+
+/* magnus_symbolic (magnus.py:420-456): writes C.row_ptr (int64, n_rows+1,
+ * device) and the total nnz(C) to *nnz_out (host; the call synchronises). */
+int magnus_symbolic(magnus_ctx* ctx, int64_t* c_row_ptr, int64_t* nnz_out, void* stream);
+
+/* magnus_numeric (magnus.py:459-542): fills C.col / C.val (device, nnz(C)
+ * entries) canonically; counters (host) as in SpgemmResult.counters. */
+int magnus_numeric(magnus_ctx* ctx, const int64_t* c_row_ptr, uint32_t* c_col, double* c_val,
+                   magnus_counters* counters, void* stream);
+
+/* row_intermediate_stats gustavson.py:97-134 on device arrays (n_rows each). */
+int magnus_row_stats(const magnus_csr* A, const magnus_csr* B, int64_t* inter, int64_t* min_col, int64_t* max_col,
+                     void* stream);
+
+/* Per-row categories (int8, MAGNUS_CAT_*) computed by the last magnus_setup; copies n_rows bytes to device dst. */
+int magnus_categories(magnus_ctx* ctx, int8_t* dst, void* stream);
+
+/* Number of kernel launches issued by this context since creation (telemetry). */
+int64_t magnus_launch_count(magnus_ctx* ctx);
+
+const char* magnus_last_error(void);
+const char* magnus_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MAGNUS_B200_H */

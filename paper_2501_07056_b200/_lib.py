@@ -1,0 +1,128 @@
+"""ctypes binding of the C-ABI in include/magnus_b200.h (libmagnus_b200.so).
+
+The shared library is built in-tree for sm_100a by `build()` (nvcc) and is the
+only compute path: there is no CPU fallback.  Loading fails loudly if it is
+missing.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+from .errors import raise_for_status
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libmagnus_b200.so")
+CSRC = os.path.join(HERE, "csrc")
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
+
+
+def sources():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh")))
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile csrc/*.cu into libmagnus_b200.so (sm_100a).  No GPU needed."""
+    srcs = sources()
+    hdr = os.path.join(ROOT, "include", "magnus_b200.h")
+    newest = max(os.path.getmtime(p) for p in srcs + [hdr])
+    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
+        return LIB_PATH
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    if not os.path.exists(nvcc):
+        nvcc = "nvcc"
+    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB_PATH + ".tmp", os.path.join(CSRC, "magnus_b200.cu")]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.check_call(cmd)
+    os.replace(LIB_PATH + ".tmp", LIB_PATH)
+    return LIB_PATH
+
+
+class Csr(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_cols", C.c_int64), ("nnz", C.c_int64), ("row_ptr", C.c_void_p),
+                ("rp_bytes", C.c_int32), ("col", C.c_void_p), ("val", C.c_void_p)]
+
+
+class Sys(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("cache_line_bytes", "l2_bytes", "memory_budget_bytes", "histo_type_bytes",
+                                         "prefix_sum_type_bytes", "val_bytes")]
+
+
+class Thresholds(C.Structure):
+    _fields_ = [("sort_dense_crossover", C.c_int64), ("sort_sweet_spot", C.c_int64)]
+
+
+class Plan(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("plan_cols", "s_dense_accum", "s_chunk_fine", "n_chunks_fine", "chunk_len_fine",
+                                         "shift_fine", "m_max_l2", "use_coarse", "n_chunks_coarse", "chunk_len_coarse",
+                                         "shift_coarse")]
+
+
+class Counters(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("nnz_c", "inter_prod_size", "coarse_batches", "rows_sort", "rows_dense",
+                                         "rows_fine", "rows_coarse")]
+
+
+# every symbol include/magnus_b200.h declares
+EXPORTS = ["magnus_compute_chunk_plan", "magnus_ctx_create", "magnus_ctx_destroy", "magnus_setup", "magnus_symbolic",
+           "magnus_numeric", "magnus_row_stats", "magnus_categories", "magnus_launch_count", "magnus_last_error",
+           "magnus_version"]
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.magnus_last_error.restype = C.c_char_p
+        L.magnus_version.restype = C.c_char_p
+        L.magnus_launch_count.restype = C.c_int64
+        L.magnus_launch_count.argtypes = [C.c_void_p]
+        L.magnus_ctx_destroy.argtypes = [C.c_void_p]
+        L.magnus_ctx_destroy.restype = None
+        L.magnus_ctx_create.argtypes = [C.POINTER(C.c_void_p)]
+        L.magnus_setup.argtypes = [C.c_void_p, C.POINTER(Csr), C.POINTER(Csr), C.POINTER(Sys), C.POINTER(Thresholds),
+                                   C.c_int, C.c_void_p]
+        L.magnus_symbolic.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
+        L.magnus_numeric.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Counters), C.c_void_p]
+        L.magnus_row_stats.argtypes = [C.POINTER(Csr), C.POINTER(Csr), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.magnus_categories.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.magnus_compute_chunk_plan.argtypes = [C.POINTER(Sys), C.c_int64, C.c_int, C.c_int, C.POINTER(Plan)]
+        _LIB = L
+    return _LIB
+
+
+def check(rc: int) -> None:
+    if rc:
+        raise_for_status(rc, lib().magnus_last_error().decode())
+
+
+class Context:
+    """Owns a magnus_ctx (device workspace between the phases)."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        check(lib().magnus_ctx_create(C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().magnus_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def launches(self) -> int:
+        return int(lib().magnus_launch_count(self.h))

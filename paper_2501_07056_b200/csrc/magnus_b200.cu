@@ -1,0 +1,425 @@
+// Host side of the C-ABI (include/magnus_b200.h): plans, launches, workspace.
+//
+// Reference boundary: spgemm_magnus / magnus_symbolic / magnus_numeric
+// (magnus.py:420-583).  One context holds the per-call device state between
+// the symbolic and numeric phases, like the reference keeps `stats`, `cats`
+// and the plans between the two calls.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/magnus_b200.h"
+#include "common.cuh"
+#include "heavy_rows.cuh"
+#include "setup_kernels.cuh"
+#include "small_rows.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define MG_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return set_err(MAGNUS_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+int64_t ceil_pow2(int64_t x) {
+  int64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+int64_t exact_log2(int64_t x) {
+  int64_t k = 0;
+  while ((int64_t(1) << k) < x) ++k;
+  return k;
+}
+// util.py:28-44
+int64_t round_pow2_of_sqrt(unsigned __int128 num, unsigned __int128 den) {
+  if (num < den) return 1;
+  int k = 0;
+  while (num >= (den << (2 * (k + 1)))) ++k;
+  if (num >= (den << (2 * k + 1))) ++k;
+  return int64_t(1) << k;
+}
+
+mg::DevCsr dev_csr(const magnus_csr& m) {
+  mg::DevCsr d;
+  d.n_rows = m.n_rows;
+  d.n_cols = m.n_cols;
+  d.nnz = m.nnz;
+  d.rp64 = m.rp_bytes == 8 ? static_cast<const int64_t*>(m.row_ptr) : nullptr;
+  d.rp32 = m.rp_bytes == 4 ? static_cast<const int32_t*>(m.row_ptr) : nullptr;
+  d.col = m.col;
+  d.val = m.val;
+  return d;
+}
+
+}  // namespace
+
+struct magnus_ctx {
+  int device = 0;
+  int sm_count = 148;
+  int64_t launches = 0;
+  std::vector<void*> allocs;   // per-setup device allocations
+  cudaStream_t stream = nullptr;
+
+  mg::DevCsr A{}, B{};
+  magnus_sys sys{};
+  magnus_thresholds th{};
+  magnus_chunk_plan plan_sym{}, plan_num{};
+  int force_fine_only = 0;
+  bool ready = false;
+  bool have_symbolic = false;
+
+  int64_t* inter = nullptr;
+  int64_t* mn = nullptr;
+  int64_t* mx = nullptr;
+  int8_t* cat = nullptr;
+  int32_t* listW = nullptr;
+  int32_t* listB = nullptr;
+  int32_t* listH = nullptr;
+  int32_t* listCoarse = nullptr;
+  unsigned long long* stats = nullptr;   // kStatLen
+  unsigned long long* work = nullptr;    // work counters (4)
+  unsigned long long* err = nullptr;
+  int64_t* counts = nullptr;
+  int64_t* tile_sums = nullptr;
+  uint32_t* modebits = nullptr;
+  uint32_t* gk = nullptr;
+  uint32_t* gchunk = nullptr;
+  int64_t gk_stride = 0;
+  int64_t host_stats[mg::kStatLen] = {0};
+  int64_t coarse_batches = 0;
+  mg::Sem sem{};
+
+  void free_all() {
+    for (void* p : allocs) cudaFreeAsync(p, stream);
+    allocs.clear();
+  }
+  template <class T>
+  cudaError_t alloc(T** p, size_t count) {
+    void* q = nullptr;
+    cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(count, 1) * sizeof(T), stream);
+    if (e == cudaSuccess) allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return e;
+  }
+};
+
+extern "C" {
+
+const char* magnus_last_error(void) { return g_err.c_str(); }
+const char* magnus_version(void) { return "magnus_b200 0.1 (sm_100a)"; }
+int64_t magnus_launch_count(magnus_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// compute_chunk_plan planner.py:106-152
+int magnus_compute_chunk_plan(const magnus_sys* sys, int64_t m_c, int numeric, int allow_coarse, magnus_chunk_plan* out) {
+  if (!sys || !out) return set_err(MAGNUS_INPUT, "null argument");
+  if (m_c < 1) return set_err(MAGNUS_INPUT, "m_c must be >= 1");
+  if (sys->cache_line_bytes <= 0 || sys->l2_bytes <= 0 || sys->memory_budget_bytes <= 0 || sys->histo_type_bytes <= 0 ||
+      sys->prefix_sum_type_bytes <= 0 || sys->val_bytes <= 0)
+    return set_err(MAGNUS_INPUT, "SystemParams fields must be positive");
+  if (sys->cache_line_bytes & (sys->cache_line_bytes - 1)) return set_err(MAGNUS_INPUT, "cache_line_bytes must be a power of two");
+  const int64_t plan_cols = ceil_pow2(m_c);
+  const int64_t sda = numeric ? sys->val_bytes + 1 : 1;
+  const int64_t scf = sys->histo_type_bytes + sys->prefix_sum_type_bytes + 2 * sys->cache_line_bytes;
+  const unsigned __int128 raw =
+      (unsigned __int128)sys->l2_bytes * (unsigned __int128)sys->l2_bytes / (unsigned __int128)(4 * scf);
+  int64_t m_max = 1;
+  if (raw >= 1) {
+    unsigned __int128 p = 1;
+    while ((p << 1) <= raw) p <<= 1;
+    m_max = (int64_t)p;
+  }
+  const int use_coarse = allow_coarse && plan_cols > m_max;
+  const int64_t span = use_coarse ? m_max : plan_cols;
+  int64_t n_fine = round_pow2_of_sqrt((unsigned __int128)span * sda, scf);
+  const int64_t min_len = std::max<int64_t>(1, sys->cache_line_bytes / 4);
+  n_fine = std::min(n_fine, std::max<int64_t>(1, span / min_len));
+  n_fine = std::max<int64_t>(1, std::min(n_fine, span));
+  const int64_t len = span / n_fine;
+  out->plan_cols = plan_cols;
+  out->s_dense_accum = sda;
+  out->s_chunk_fine = scf;
+  out->n_chunks_fine = n_fine;
+  out->chunk_len_fine = len;
+  out->shift_fine = exact_log2(len);
+  out->m_max_l2 = m_max;
+  out->use_coarse = use_coarse;
+  out->n_chunks_coarse = use_coarse ? plan_cols / m_max : 1;
+  out->chunk_len_coarse = use_coarse ? m_max : plan_cols;
+  out->shift_coarse = exact_log2(out->chunk_len_coarse);
+  return MAGNUS_OK;
+}
+
+int magnus_ctx_create(magnus_ctx** out) {
+  if (!out) return set_err(MAGNUS_INPUT, "null argument");
+  auto* c = new magnus_ctx();
+  MG_CUDA(cudaGetDevice(&c->device));
+  MG_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_rows_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mg::kBSmem));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_rows_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mg::kBSmem));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_heavy_symbolic, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)mg::HeavySymSmem::kTotal));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_heavy_numeric, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)mg::HeavyNumSmem::kTotal));
+  *out = c;
+  return MAGNUS_OK;
+}
+
+void magnus_ctx_destroy(magnus_ctx* ctx) {
+  if (!ctx) return;
+  ctx->free_all();
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  delete ctx;
+}
+
+int magnus_row_stats(const magnus_csr* A, const magnus_csr* B, int64_t* inter, int64_t* min_col, int64_t* max_col,
+                     void* stream) {
+  if (!A || !B) return set_err(MAGNUS_INPUT, "null argument");
+  if (A->n_cols != B->n_rows) return set_err(MAGNUS_INPUT, "dimension mismatch");
+  if (A->n_rows == 0) return MAGNUS_OK;
+  int dev = 0, sms = 148;
+  MG_CUDA(cudaGetDevice(&dev));
+  MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t warps = std::min<int64_t>(A->n_rows, (int64_t)sms * 64);
+  mg::k_row_stats<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(dev_csr(*A), dev_csr(*B), inter,
+                                                                                         min_col, max_col);
+  MG_CUDA(cudaGetLastError());
+  return MAGNUS_OK;
+}
+
+int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, const magnus_sys* sys,
+                 const magnus_thresholds* th, int force_fine_only, void* stream) {
+  if (!ctx || !A || !B || !sys || !th) return set_err(MAGNUS_INPUT, "null argument");
+  if (A->n_cols != B->n_rows)   // _check_dims gustavson.py:39-41
+    return set_err(MAGNUS_INPUT, "dimension mismatch: A is " + std::to_string(A->n_rows) + "x" + std::to_string(A->n_cols) +
+                                     ", B is " + std::to_string(B->n_rows) + "x" + std::to_string(B->n_cols));
+  if ((A->rp_bytes != 4 && A->rp_bytes != 8) || (B->rp_bytes != 4 && B->rp_bytes != 8))
+    return set_err(MAGNUS_INPUT, "row_ptr must be int32 or int64");
+  if (B->nnz >= (int64_t(1) << 32) || A->n_rows >= (int64_t(1) << 31))
+    return set_err(MAGNUS_INPUT, "device limits: nnz(B) < 2^32 and n_rows(A) < 2^31");
+  if (B->n_cols > (int64_t(1) << 32)) return set_err(MAGNUS_INPUT, "more than 2^32 columns needs 8-byte column indices");
+  if (th->sort_dense_crossover < 1 || th->sort_sweet_spot > th->sort_dense_crossover)
+    return set_err(MAGNUS_INPUT, "invalid AccumThresholds");
+  if (th->sort_dense_crossover > mg::kCap)
+    return set_err(MAGNUS_INPUT, "sort_dense_crossover above the device batch capacity (8192)");
+  ctx->free_all();
+  ctx->stream = (cudaStream_t)stream;
+  cudaStream_t s = ctx->stream;
+  ctx->A = dev_csr(*A);
+  ctx->B = dev_csr(*B);
+  ctx->sys = *sys;
+  ctx->th = *th;
+  ctx->force_fine_only = force_fine_only;
+  ctx->ready = false;
+  ctx->have_symbolic = false;
+  const int64_t m_c = std::max<int64_t>(B->n_cols, 1);   // magnus.py:565
+  int rc = magnus_compute_chunk_plan(sys, m_c, 0, !force_fine_only, &ctx->plan_sym);
+  if (rc) return rc;
+  rc = magnus_compute_chunk_plan(sys, m_c, 1, !force_fine_only, &ctx->plan_num);
+  if (rc) return rc;
+  const int64_t n = A->n_rows;
+  MG_CUDA(ctx->alloc(&ctx->inter, n + 1));
+  MG_CUDA(ctx->alloc(&ctx->mn, n + 1));
+  MG_CUDA(ctx->alloc(&ctx->mx, n + 1));
+  MG_CUDA(ctx->alloc(&ctx->cat, n + 1));
+  MG_CUDA(ctx->alloc(&ctx->listW, n + 1));
+  MG_CUDA(ctx->alloc(&ctx->listB, n + 1));
+  MG_CUDA(ctx->alloc(&ctx->listH, n + 1));
+  MG_CUDA(ctx->alloc(&ctx->listCoarse, n + 1));
+  MG_CUDA(ctx->alloc(&ctx->stats, mg::kStatLen));
+  MG_CUDA(ctx->alloc(&ctx->work, 8));
+  MG_CUDA(ctx->alloc(&ctx->err, 2));
+  MG_CUDA(cudaMemsetAsync(ctx->stats, 0, mg::kStatLen * 8, s));
+  MG_CUDA(cudaMemsetAsync(ctx->err, 0, 16, s));
+  if (n > 0) {
+    rc = magnus_row_stats(A, B, ctx->inter, ctx->mn, ctx->mx, stream);
+    if (rc) return rc;
+    ++ctx->launches;
+    mg::CatParams cp{th->sort_dense_crossover, sys->l2_bytes, sys->val_bytes, (int32_t)ctx->plan_sym.use_coarse};
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sm_count * 16);
+    mg::k_categorize<<<grid, 256, 0, s>>>(n, ctx->A, ctx->inter, ctx->mn, ctx->mx, cp, ctx->cat, ctx->listW, ctx->listB,
+                                          ctx->listH, ctx->listCoarse, ctx->stats);
+    MG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+  }
+  unsigned long long hs[mg::kStatLen];
+  MG_CUDA(cudaMemcpyAsync(hs, ctx->stats, sizeof hs, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  for (int j = 0; j < mg::kStatLen; ++j) ctx->host_stats[j] = (int64_t)hs[j];
+  // build_coarse_batches (magnus.py:277-314): batch count and the over-budget error.
+  ctx->coarse_batches = 0;
+  const int64_t ncoarse = ctx->host_stats[mg::kStatNCoarse];
+  if (ncoarse > 0) {
+    std::vector<int32_t> rows(ncoarse);
+    MG_CUDA(cudaMemcpyAsync(rows.data(), ctx->listCoarse, ncoarse * 4, cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    std::sort(rows.begin(), rows.end());
+    std::vector<int64_t> inter(ncoarse);
+    for (int64_t j = 0; j < ncoarse; ++j)
+      MG_CUDA(cudaMemcpyAsync(&inter[j], ctx->inter + rows[j], 8, cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    const int64_t ncc = ctx->plan_sym.n_chunks_coarse, budget = sys->memory_budget_bytes;
+    const int64_t bpe = (B->n_cols <= (int64_t(1) << 32) ? 4 : 8) + sys->val_bytes;   // magnus.py:414-417
+    int64_t cur_n = 0, cur_bytes = 0, cur_meta = 0, nb = 0;
+    for (int64_t j = 0; j < ncoarse; ++j) {
+      const int64_t isz = inter[j], row_bytes = isz * bpe;
+      if (row_bytes > budget)
+        return set_err(MAGNUS_OVER_BUDGET, "row " + std::to_string(rows[j]) + ": buffering " + std::to_string(isz) +
+                                               " intermediate elements needs " + std::to_string(row_bytes) +
+                                               " bytes, over the " + std::to_string(budget) + "-byte memory budget");
+      const int64_t meta = ncc * sys->histo_type_bytes + (ncc + 1) * sys->prefix_sum_type_bytes +
+                           2 * sys->cache_line_bytes * std::min(ncc, isz);
+      if (cur_n && (cur_bytes + row_bytes > budget || cur_meta + meta > sys->l2_bytes)) {
+        ++nb;
+        cur_n = cur_bytes = cur_meta = 0;
+      }
+      ++cur_n;
+      cur_bytes += row_bytes;
+      cur_meta += meta;
+    }
+    if (cur_n) ++nb;
+    ctx->coarse_batches = nb;
+  }
+  // device semantics
+  ctx->sem.crossover = th->sort_dense_crossover;
+  ctx->sem.shift_num = (int32_t)ctx->plan_num.shift_fine;
+  // numeric-plan fine chunks over the whole column span (n_fine per coarse chunk x n_coarse):
+  // the chunk of column c is c >> shift_fine in both the fine and the coarse level.
+  const int64_t n_chunks_global = ctx->plan_num.plan_cols >> ctx->plan_num.shift_fine;
+  ctx->sem.n_chunks_num = n_chunks_global;
+  ctx->sem.mode_words = (int32_t)((n_chunks_global + 31) / 32);
+  // heavy-row workspace
+  const int64_t nH = ctx->host_stats[mg::kStatNH];
+  MG_CUDA(ctx->alloc(&ctx->modebits, std::max<int64_t>(1, nH) * ctx->sem.mode_words));
+  const int64_t maxnk = ctx->host_stats[mg::kStatMaxNk];
+  ctx->gk_stride = maxnk > mg::kKS ? ((maxnk + 8) / 4) * 4 : 4;
+  MG_CUDA(ctx->alloc(&ctx->gk, (size_t)ctx->sm_count * ctx->gk_stride * 6));
+  const bool chunk_global = n_chunks_global > mg::kChunkSmem;
+  MG_CUDA(ctx->alloc(&ctx->gchunk, chunk_global ? (size_t)ctx->sm_count * n_chunks_global : 1));
+  if (chunk_global) MG_CUDA(cudaMemsetAsync(ctx->gchunk, 0, (size_t)ctx->sm_count * n_chunks_global * 4, s));
+  MG_CUDA(ctx->alloc(&ctx->counts, n + 1));
+  MG_CUDA(ctx->alloc(&ctx->tile_sums, (n + mg::kScanTile - 1) / mg::kScanTile + 1));
+  ctx->ready = true;
+  return MAGNUS_OK;
+}
+
+int magnus_categories(magnus_ctx* ctx, int8_t* dst, void* stream) {
+  if (!ctx || !ctx->ready) return set_err(MAGNUS_CONTRACT, "magnus_setup has not run");
+  if (ctx->A.n_rows) MG_CUDA(cudaMemcpyAsync(dst, ctx->cat, ctx->A.n_rows, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return MAGNUS_OK;
+}
+
+static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint32_t* c_col, double* c_val) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nW = ctx->host_stats[mg::kStatNW], nB = ctx->host_stats[mg::kStatNB], nH = ctx->host_stats[mg::kStatNH];
+  if (nH > 0) {
+    MG_CUDA(cudaMemsetAsync(ctx->work, 0, 8, s));
+    const unsigned grid = (unsigned)std::min<int64_t>(nH, ctx->sm_count);
+    if (numeric)
+      mg::k_heavy_numeric<<<grid, mg::kHT, mg::HeavyNumSmem::kTotal, s>>>(
+          ctx->A, ctx->B, ctx->listH, nH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->modebits, c_rp, c_col, c_val, ctx->gk,
+          ctx->gk_stride, ctx->work, ctx->err);
+    else
+      mg::k_heavy_symbolic<<<grid, mg::kHT, mg::HeavySymSmem::kTotal, s>>>(
+          ctx->A, ctx->B, ctx->listH, nH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->counts, ctx->modebits, ctx->gk,
+          ctx->gk_stride, ctx->gchunk, ctx->work);
+    MG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+  }
+  if (nB > 0) {
+    const unsigned grid = (unsigned)std::min<int64_t>(nB, (int64_t)ctx->sm_count * 3);
+    if (numeric)
+      mg::k_rows_block<true><<<grid, mg::kBT, mg::kBSmem, s>>>(ctx->A, ctx->B, ctx->listB, nB, ctx->cat, ctx->sem,
+                                                                ctx->counts, c_rp, c_col, c_val, ctx->err);
+    else
+      mg::k_rows_block<false><<<grid, mg::kBT, mg::kBSmem, s>>>(ctx->A, ctx->B, ctx->listB, nB, ctx->cat, ctx->sem,
+                                                                 ctx->counts, c_rp, c_col, c_val, ctx->err);
+    MG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+  }
+  if (nW > 0) {
+    const int64_t blocks = (nW + mg::kWT / 32 - 1) / (mg::kWT / 32);
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks, (int64_t)ctx->sm_count * 8);
+    if (numeric)
+      mg::k_rows_warp<true><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts, c_rp,
+                                                      c_col, c_val, ctx->err);
+    else
+      mg::k_rows_warp<false><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts,
+                                                       c_rp, c_col, c_val, ctx->err);
+    MG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+  }
+  return MAGNUS_OK;
+}
+
+int magnus_symbolic(magnus_ctx* ctx, int64_t* c_row_ptr, int64_t* nnz_out, void* stream) {
+  if (!ctx || !ctx->ready) return set_err(MAGNUS_CONTRACT, "magnus_setup has not run");
+  ctx->stream = (cudaStream_t)stream;
+  cudaStream_t s = ctx->stream;
+  const int64_t n = ctx->A.n_rows;
+  if (n == 0) {
+    MG_CUDA(cudaMemsetAsync(c_row_ptr, 0, 8, s));
+    if (nnz_out) *nnz_out = 0;
+    ctx->have_symbolic = true;
+    return MAGNUS_OK;
+  }
+  MG_CUDA(cudaMemsetAsync(ctx->counts, 0, n * 8, s));   // rows with an empty product stay 0
+  int rc = launch_rows(ctx, false, nullptr, nullptr, nullptr);
+  if (rc) return rc;
+  // row_ptr = cumsum(counts)  (magnus.py:454-456)
+  const int64_t tiles = (n + mg::kScanTile - 1) / mg::kScanTile;
+  mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->counts, n, ctx->tile_sums);
+  mg::k_scan_tiles<<<1, 1024, 0, s>>>(ctx->tile_sums, tiles);
+  mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->counts, n, ctx->tile_sums, c_row_ptr);
+  MG_CUDA(cudaGetLastError());
+  ctx->launches += 3;
+  int64_t nnz = 0;
+  MG_CUDA(cudaMemcpyAsync(&nnz, c_row_ptr + n, 8, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  if (nnz_out) *nnz_out = nnz;
+  ctx->have_symbolic = true;
+  return MAGNUS_OK;
+}
+
+int magnus_numeric(magnus_ctx* ctx, const int64_t* c_row_ptr, uint32_t* c_col, double* c_val, magnus_counters* counters,
+                   void* stream) {
+  if (!ctx || !ctx->ready) return set_err(MAGNUS_CONTRACT, "magnus_setup has not run");
+  if (!ctx->have_symbolic) return set_err(MAGNUS_CONTRACT, "row_ptr does not come from a symbolic pass of (A, B)");
+  ctx->stream = (cudaStream_t)stream;
+  cudaStream_t s = ctx->stream;
+  if (ctx->A.n_rows > 0) {
+    int rc = launch_rows(ctx, true, c_row_ptr, c_col, c_val);
+    if (rc) return rc;
+  }
+  unsigned long long e = 0;
+  MG_CUDA(cudaMemcpyAsync(&e, ctx->err, 8, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  if (e) return set_err(MAGNUS_CONTRACT, "numeric phase count differs from the symbolic count");
+  if (counters) {
+    int64_t nnz = 0;
+    if (ctx->A.n_rows > 0) MG_CUDA(cudaMemcpy(&nnz, c_row_ptr + ctx->A.n_rows, 8, cudaMemcpyDeviceToHost));
+    counters->nnz_c = nnz;
+    counters->inter_prod_size = ctx->host_stats[mg::kStatInter];
+    counters->coarse_batches = ctx->coarse_batches;
+    counters->rows_sort = ctx->host_stats[mg::kStatCat + 0];
+    counters->rows_dense = ctx->host_stats[mg::kStatCat + 1];
+    counters->rows_fine = ctx->host_stats[mg::kStatCat + 2];
+    counters->rows_coarse = ctx->host_stats[mg::kStatCat + 3];
+  }
+  return MAGNUS_OK;
+}
+
+}  // extern "C"

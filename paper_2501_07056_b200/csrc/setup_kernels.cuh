@@ -1,0 +1,191 @@
+// Setup-phase kernels: row statistics, categorisation / binning, device-wide scan.
+#pragma once
+#include "common.cuh"
+
+namespace mg {
+
+// row_intermediate_stats (reference gustavson.py:97-134): one warp per row.
+// inter[i] = sum of nnz(B_k) over k in A_i; [min_col, max_col] spans the first /
+// last column of every referenced non-empty B row; empty product -> (0, 0, -1).
+__global__ void k_row_stats(DevCsr A, DevCsr B, int64_t* __restrict__ inter, int64_t* __restrict__ mn,
+                            int64_t* __restrict__ mx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < A.n_rows; i += nwarps) {
+    const int64_t a0 = A.rp(i), a1 = A.rp(i + 1);
+    int64_t s = 0, lo = INT64_MAX, hi = -1;
+    for (int64_t t = a0 + lane; t < a1; t += 32) {
+      const int64_t k = __ldg(A.col + t);
+      const int64_t b0 = B.rp(k), b1 = B.rp(k + 1);
+      s += b1 - b0;
+      if (b1 > b0) {
+        const int64_t f = __ldg(B.col + b0), l = __ldg(B.col + b1 - 1);
+        lo = f < lo ? f : lo;
+        hi = l > hi ? l : hi;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      int64_t l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+      lo = l2 < lo ? l2 : lo;
+      hi = h2 > hi ? h2 : hi;
+    }
+    if (lane == 0) {
+      inter[i] = s;
+      mn[i] = s > 0 ? lo : 0;
+      mx[i] = s > 0 ? hi : -1;
+    }
+  }
+}
+
+// Device row classes (execution strategy only; results never depend on them).
+constexpr int kClsNone = -1, kClsWarp = 0, kClsBlock = 1, kClsHeavy = 2;
+constexpr int64_t kWarpMax = 256;    // <= 256 intermediate elements: one warp, smem bitonic
+constexpr int64_t kBlockMax = 4096;  // <= 4096: one CTA, smem bitonic
+
+struct CatParams {
+  int64_t crossover;   // sort_dense_crossover
+  int64_t l2_bytes;    // SystemParams.l2_bytes
+  int64_t val_bytes;   // SystemParams.val_bytes
+  int32_t use_coarse;  // symbolic ChunkPlan.use_coarse
+};
+
+// stats layout (int64): [0..3] rows per category, [4] sum inter, [5] max nk of heavy rows,
+// [6] nW, [7] nB, [8] nH, [9] error flag, [10] n coarse rows
+constexpr int kStatCat = 0, kStatInter = 4, kStatMaxNk = 5, kStatNW = 6, kStatNB = 7, kStatNH = 8, kStatErr = 9,
+              kStatNCoarse = 10, kStatLen = 16;
+
+// categorize_rows (reference magnus.py:68-94): first matching rule wins.
+// Also bins rows into the device execution classes and lists coarse rows.
+__global__ void k_categorize(int64_t n, DevCsr A, const int64_t* __restrict__ inter, const int64_t* __restrict__ mn,
+                             const int64_t* __restrict__ mx, CatParams p, int8_t* __restrict__ cat,
+                             int32_t* __restrict__ listW, int32_t* __restrict__ listB, int32_t* __restrict__ listH,
+                             int32_t* __restrict__ listCoarse, unsigned long long* __restrict__ stats) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = inter[i];
+    const int64_t range = mx[i] - mn[i] + 1;
+    int c;
+    if (s < p.crossover) c = kCatSort;
+    else if (range * (p.val_bytes + 1) <= p.l2_bytes) c = kCatDense;
+    else c = p.use_coarse ? kCatCoarse : kCatFine;
+    cat[i] = (int8_t)c;
+    atomicAdd(&stats[kStatCat + c], 1ull);
+    atomicAdd(&stats[kStatInter], (unsigned long long)s);
+    if (c == kCatCoarse) {
+      unsigned long long slot = atomicAdd(&stats[kStatNCoarse], 1ull);
+      listCoarse[slot] = (int32_t)i;
+    }
+    if (s == 0) continue;
+    if (s <= kWarpMax) {
+      listW[atomicAdd(&stats[kStatNW], 1ull)] = (int32_t)i;
+    } else if (s <= kBlockMax) {
+      listB[atomicAdd(&stats[kStatNB], 1ull)] = (int32_t)i;
+    } else {
+      listH[atomicAdd(&stats[kStatNH], 1ull)] = (int32_t)i;
+      atomicMax(&stats[kStatMaxNk], (unsigned long long)(A.rp(i + 1) - A.rp(i)));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- device-wide exclusive scan (int64)
+constexpr int kScanT = 512, kScanItems = 16, kScanTile = kScanT * kScanItems;
+
+__global__ void k_scan_reduce(const int64_t* __restrict__ in, int64_t n, int64_t* __restrict__ tile_sums) {
+  __shared__ int64_t sh[kScanT / 32];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  int64_t s = 0;
+  for (int j = 0; j < kScanItems; ++j) {
+    int64_t idx = base + (int64_t)j * kScanT + threadIdx.x;
+    if (idx < n) s += in[idx];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < kScanT / 32; ++w) t += sh[w];
+    tile_sums[blockIdx.x] = t;
+  }
+}
+
+// exclusive scan of tile sums in place (single block, any count)
+__global__ void k_scan_tiles(int64_t* __restrict__ tile_sums, int64_t ntiles) {
+  __shared__ int64_t sh[33];
+  int64_t carry = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t base = 0; base < ntiles; base += blockDim.x) {
+    int64_t idx = base + threadIdx.x;
+    int64_t v = idx < ntiles ? tile_sums[idx] : 0;
+    int64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) sh[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      int64_t w = lane < (int)(blockDim.x / 32) ? sh[lane] : 0;
+      int64_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += t;
+      }
+      if (lane < (int)(blockDim.x / 32)) sh[lane] = wi - w;
+      if (lane == 31) sh[32] = wi;
+    }
+    __syncthreads();
+    if (idx < ntiles) tile_sums[idx] = carry + sh[wid] + inc - v;
+    carry += sh[32];
+    __syncthreads();
+  }
+}
+
+// out[i] = exclusive prefix of in (out has n+1 entries; out[n] = total)
+__global__ void k_scan_apply(const int64_t* __restrict__ in, int64_t n, const int64_t* __restrict__ tile_sums,
+                             int64_t* __restrict__ out) {
+  __shared__ int64_t sh[33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  int64_t v[kScanItems];
+  int64_t s = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    int64_t idx = base + j;
+    v[j] = idx < n ? in[idx] : 0;
+    s += v[j];
+  }
+  int64_t inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) sh[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t w = lane < kScanT / 32 ? sh[lane] : 0;
+    int64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < kScanT / 32) sh[lane] = wi - w;
+  }
+  __syncthreads();
+  int64_t run = tile_sums[blockIdx.x] + sh[wid] + inc - s;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    int64_t idx = base + j;
+    if (idx < n) out[idx] = run;
+    run += v[j];
+    if (idx == n - 1) out[n] = run;
+  }
+}
+
+}  // namespace mg

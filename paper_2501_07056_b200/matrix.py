@@ -84,6 +84,7 @@ def validate_csr(m: CsrMatrix) -> None:
             raise InputError("column index out of range")
         if m.canonical:
             inner = np.diff(c)
-            inner[rp[1:-1][rp[1:-1] > 0] - 1] = 1
+            idx = rp[1:-1] - 1
+            inner[idx[(idx >= 0) & (idx < inner.size)]] = 1
             if inner.size and inner.min() <= 0:
                 raise InputError("columns not strictly increasing within a row")

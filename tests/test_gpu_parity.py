@@ -1,0 +1,126 @@
+"""Parity of the CUDA path (through the C-ABI) with the reference.
+
+* every golden run of the unmodified reference (tests/golden/) -- bit-exact C
+  (row_ptr, col, value bits), identical counters, identical errors;
+* larger seeded inputs against the pinned CPU oracle, bit-exact, across
+  SystemParams that force every category and every device kernel
+  (warp / CTA / heavy-window rows, multi-batch windows, >1024-k rows).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle  # noqa: E402
+from paper_2501_07056_b200 import (AccumThresholds, CsrMatrix, OverBudgetError, SystemParams, generate,  # noqa: E402
+                                   spgemm_magnus)
+
+from golden_util import expected, inputs, runs, system  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+RUNS = runs()
+B200 = SystemParams(cache_line_bytes=128, l2_bytes=232448, memory_budget_bytes=1 << 31)
+HOST2M = SystemParams(cache_line_bytes=64, l2_bytes=2 << 20, memory_budget_bytes=1 << 31)
+FINE4K = SystemParams(cache_line_bytes=64, l2_bytes=4096)
+COARSE = SystemParams(cache_line_bytes=64, l2_bytes=1400)
+
+
+def assert_same(res, ref):
+    np.testing.assert_array_equal(np.asarray(res.C.row_ptr), ref.row_ptr)
+    np.testing.assert_array_equal(np.asarray(res.C.col), ref.col)
+    np.testing.assert_array_equal(np.asarray(res.C.val).view(np.uint64), ref.val.view(np.uint64))
+    assert res.counters == ref.counters
+
+
+@pytest.mark.parametrize("rec", RUNS, ids=[f"{r['case']}-{r['sys']}-{int(r.get('force_fine_only', 0))}" for r in RUNS])
+def test_reference_golden(rec):
+    A, B = inputs(rec["case"])
+    sysp = system(rec["sys"], rec)
+    if rec.get("error"):
+        with pytest.raises(OverBudgetError):
+            spgemm_magnus(A, B, sys=sysp, force_fine_only=rec.get("force_fine_only", False))
+        return
+    res = spgemm_magnus(A, B, sys=sysp, force_fine_only=rec["force_fine_only"])
+    rp, col, val = expected(rec)
+    np.testing.assert_array_equal(res.C.row_ptr, rp)
+    np.testing.assert_array_equal(res.C.col, col)
+    np.testing.assert_array_equal(res.C.val.view(np.uint64), val.view(np.uint64))
+    assert res.counters == rec["counters"]
+
+
+def _hub_matrix(n=4096, heavy_rows=6, heavy_deg=3000, seed=9):
+    """R-MAT body plus a few rows with > 1024 nonzeros and dense hub B rows:
+    exercises the global-cursor path, multi-batch windows and narrowing."""
+    R = generate.rmat(12, 16, seed=seed)
+    rng = np.random.default_rng(seed)
+    rows = []
+    rp = np.asarray(R.row_ptr)
+    for i in range(n):
+        r = np.asarray(R.col[rp[i]:rp[i + 1]], dtype=np.int64)
+        if i < heavy_rows:
+            r = np.union1d(r, rng.choice(n, size=heavy_deg, replace=False))
+        if 10 <= i < 14:  # dense-ish hub rows of B
+            r = np.union1d(r, np.arange(0, n, 2))
+        rows.append(r)
+    rp2 = np.zeros(n + 1, np.int64)
+    np.cumsum([len(r) for r in rows], out=rp2[1:])
+    col = np.concatenate(rows).astype(np.int32)
+    val = generate.uniform_pm1(seed, 0xAB, np.arange(col.size, dtype=np.uint64))
+    return CsrMatrix(n, n, rp2, col, val)
+
+
+CASES = {
+    "rmat14": lambda: (generate.rmat(14, 16, seed=31),) * 2,
+    "hub": lambda: (_hub_matrix(),) * 2,
+    "uniform": lambda: (generate.uniform_rows(8192, 8192, 16, seed=1),) * 2,
+    "stencil": lambda: (generate.stencil27(20),) * 2,
+    "AB": lambda: (generate.uniform_rows(4096, 1 << 16, 8, seed=2), generate.uniform_rows(1 << 16, 1 << 20, 8, seed=3)),
+}
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("sysname", ["b200", "host2m", "fine4k", "coarse"])
+def test_against_oracle(case, sysname):
+    A, B = CASES[case]()
+    sysp = {"b200": B200, "host2m": HOST2M, "fine4k": FINE4K, "coarse": COARSE}[sysname]
+    ref = oracle.spgemm(A, B, sysp)
+    res = spgemm_magnus(A, B, sys=sysp)
+    assert_same(res, ref)
+
+
+def test_force_fine_only_and_thresholds():
+    A = generate.rmat(13, 16, seed=4)
+    ref = oracle.spgemm(A, A, COARSE, force_fine_only=True)
+    assert_same(spgemm_magnus(A, A, sys=COARSE, force_fine_only=True), ref)
+    th = AccumThresholds(sort_dense_crossover=64, sort_sweet_spot=8)
+    ref = oracle.spgemm(A, A, FINE4K, thresholds=th)
+    assert_same(spgemm_magnus(A, A, sys=FINE4K, thresholds=th), ref)
+
+
+def test_device_tensors_int32_row_ptr_and_determinism():
+    A = generate.rmat(13, 16, seed=5)
+    dev = torch.device("cuda")
+    Ad = CsrMatrix(A.n_rows, A.n_cols, torch.from_numpy(A.row_ptr.astype(np.int32)).to(dev),
+                   torch.from_numpy(A.col).to(dev), torch.from_numpy(A.val).to(dev))
+    r1 = spgemm_magnus(Ad, Ad, sys=B200)
+    r2 = spgemm_magnus(Ad, Ad, sys=B200)
+    assert r1.C.col.is_cuda
+    assert torch.equal(r1.C.row_ptr, r2.C.row_ptr) and torch.equal(r1.C.col, r2.C.col)
+    assert torch.equal(r1.C.val.view(torch.int64), r2.C.val.view(torch.int64))
+    ref = oracle.spgemm(A, A, B200)
+    np.testing.assert_array_equal(r1.C.row_ptr.cpu().numpy(), ref.row_ptr)
+    np.testing.assert_array_equal(r1.C.val.cpu().numpy().view(np.uint64), ref.val.view(np.uint64))
+
+
+def test_edge_shapes():
+    E = CsrMatrix(3, 5, np.zeros(4, np.int64), np.empty(0, np.int32), np.empty(0))
+    F = generate.uniform_rows(5, 7, 3, seed=1)
+    r = spgemm_magnus(E, F, sys=B200)
+    assert r.C.nnz == 0 and list(r.C.row_ptr) == [0, 0, 0, 0]
+    Z = CsrMatrix(0, 5, np.zeros(1, np.int64), np.empty(0, np.int32), np.empty(0))
+    r = spgemm_magnus(Z, F, sys=B200)
+    assert r.C.n_rows == 0 and r.C.nnz == 0
+    with pytest.raises(Exception):
+        spgemm_magnus(F, F, sys=B200)   # 5x7 . 5x7: dimension mismatch -> InputError
