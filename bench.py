@@ -1,0 +1,489 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MAGNUS SpGEMM path (BASELINE.json metric: SpGEMM GFLOP/s,
+2 x multiplications, plus achieved HBM GB/s against the roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 3] [--impl ours|reference]
+
+One "step" = one full spgemm_magnus(A, B) (setup + symbolic + numeric, C
+materialised in HBM) on the config's seeded synthetic inputs.  Multi-GPU
+(torchrun, one rank per GPU): rows of A are split into contiguous blocks of
+equal flop count, B is broadcast from rank 0 over NCCL, each rank computes its
+C row block; value = all products / max-over-ranks time (strong scaling).
+
+Prints ONE JSON line on rank 0.  --impl reference times the reference
+algorithm's CPU restatement (oracle/, the reference is pure Python and cannot
+travel to the GPU box) on a bounded row sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+# C of cfg3 is ~116 GB: avoid caching-allocator fragmentation between steps
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0   # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def hbm_peak():
+    try:
+        with open(MEASURED) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+def config_desc(cfg):
+    from paper_2501_07056_b200.generate import CONFIGS
+    p = CONFIGS[cfg]
+    names = {1: "cfg1 C=A.A uniform n=16384 16/row", 2: "cfg2 C=A.A 27-pt stencil 64^3",
+             3: "cfg3 C=A.A R-MAT 2^20 ef16 (.57,.19,.19,.05)", 4: "cfg4 C=A.B uniform 2^23 8/row",
+             5: "cfg5 C=A.A R-MAT 2^24 ef32"}
+    return names[cfg], p
+
+
+def row_block(A, lo, hi):
+    """Rows [lo, hi) of a device CSR as a CSR view (row_ptr rebased)."""
+    from paper_2501_07056_b200 import CsrMatrix
+    rp = A.row_ptr
+    a0, a1 = int(rp[lo]), int(rp[hi])
+    return CsrMatrix(hi - lo, A.n_cols, (rp[lo:hi + 1] - a0).contiguous(), A.col[a0:a1], A.val[a0:a1])
+
+
+def flop_split(inter, world):
+    """Contiguous row cuts with ~equal sum(inter) per rank."""
+    import torch
+    cs = torch.cumsum(inter, 0)
+    total = int(cs[-1]) if cs.numel() else 0
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(int(torch.searchsorted(cs, torch.tensor(total * r // world, device=cs.device))))
+    cuts.append(int(inter.numel()))
+    return cuts, total
+
+
+def broadcast_csr(M, src, device):
+    import torch
+    import torch.distributed as dist
+    from paper_2501_07056_b200 import CsrMatrix
+    meta = torch.tensor([M.n_rows, M.n_cols, M.col.numel(), 1 if M.row_ptr.dtype == torch.int64 else 0]
+                        if M is not None else [0, 0, 0, 0], dtype=torch.int64, device=device)
+    dist.broadcast(meta, src)
+    n, m, nnz, rp64 = (int(x) for x in meta.tolist())
+    if M is None:
+        M = CsrMatrix(n, m, torch.empty(n + 1, dtype=torch.int64 if rp64 else torch.int32, device=device),
+                      torch.empty(nnz, dtype=torch.int32, device=device),
+                      torch.empty(nnz, dtype=torch.float64, device=device))
+    for t in (M.row_ptr, M.col, M.val):
+        dist.broadcast(t, src)
+    return M
+
+
+def algorithmic_bytes(A, B, inter, c_nnz_row, rp_bytes_a, rp_bytes_b):
+    """Per device row class: (symbolic bytes, numeric bytes) -- reads of A, of the B rows each
+    product touches (row_ptr pair + col [+ val]), and (numeric) the C row written.  The §8(d)
+    compulsory model restricted to the rows a kernel processes."""
+    import torch
+    nk = (A.row_ptr[1:] - A.row_ptr[:-1]).to(torch.int64)
+    classes = {"warp": (inter > 0) & (inter <= 256), "block": (inter > 256) & (inter <= 4096), "heavy": inter > 4096}
+    out = {}
+    for name, m in classes.items():
+        nkm = int(nk[m].sum())
+        im = int(inter[m].sum())
+        cm = int(c_nnz_row[m].sum())
+        rows = int(m.sum())
+        a_bytes = rows * 2 * rp_bytes_a + nkm * 12
+        b_rp = nkm * 2 * rp_bytes_b
+        sym = a_bytes - nkm * 8 + b_rp + im * 4 + rows * 8
+        num = a_bytes + b_rp + im * 12 + cm * 12 + rows * 16
+        out[name] = {"rows": rows, "inter": im, "nnz_c": cm, "sym_bytes": sym, "num_bytes": num}
+    return out
+
+
+def compulsory_bytes(n_a, nnz_a, n_inter, nnz_c, rp_a, rp_b, rp_c, n_c):
+    """A once + each product's B row (rp pair + col,val) + C once."""
+    return ((n_a + 1) * rp_a + nnz_a * 12) + (2 * nnz_a * rp_b + n_inter * 12) + ((n_c + 1) * rp_c + nnz_c * 12)
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle port)
+def cpu_baseline(A_host, B_host, sysp, seconds, inter_host, seed=0):
+    """Oracle (reference restated in C, OpenMP over rows) on a random row sample of the same
+    workload, sized for ~`seconds` of CPU work; rate = 2*sum(inter of sample)/time."""
+    from oracle import oracle
+    from paper_2501_07056_b200 import CsrMatrix
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(seed)
+    n = A_host.n_rows
+    rp = np.asarray(A_host.row_ptr, dtype=np.int64)
+
+    def sub(rows):
+        rows = np.sort(rows)
+        lens = rp[rows + 1] - rp[rows]
+        srp = np.zeros(rows.size + 1, np.int64)
+        np.cumsum(lens, out=srp[1:])
+        idx = np.concatenate([np.arange(rp[r], rp[r + 1]) for r in rows]) if rows.size else np.empty(0, np.int64)
+        return CsrMatrix(rows.size, A_host.n_cols, srp, np.asarray(A_host.col)[idx], np.asarray(A_host.val)[idx]), rows
+
+    order = rng.permutation(n)
+    # calibration on a small sample
+    csum = np.cumsum(inter_host[order])
+    target = 2e7
+    k = int(np.searchsorted(csum, target)) + 1
+    As, rows = sub(order[:k])
+    t = time.perf_counter()
+    oracle.spgemm(As, B_host, sysp, threads=threads)
+    dt = time.perf_counter() - t
+    rate = max(inter_host[rows].sum(), 1) / max(dt, 1e-6)
+    target = min(rate * seconds, float(csum[-1]))
+    k = int(np.searchsorted(csum, target)) + 1
+    As, rows = sub(order[:min(k, n)])
+    t = time.perf_counter()
+    oracle.spgemm(As, B_host, sysp, threads=threads)
+    dt = time.perf_counter() - t
+    s_inter = int(inter_host[rows].sum())
+    return {"value": 2.0 * s_inter / dt / 1e9, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+            "sample": f"{rows.size} random rows of A ({s_inter} of {int(csum[-1])} products), full symbolic+numeric, "
+                      f"{dt:.1f} s on {threads} host threads"}
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2501_07056_b200 import MagnusPlan, _lib, detect_device_params, generate, row_intermediate_stats
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=device)
+    _lib.build()
+    cfg = args.config
+    name, p = config_desc(cfg)
+
+    # inputs: rank 0 generates on its GPU, B broadcast over NCCL to the others
+    t_gen = time.perf_counter()
+    if rank == 0:
+        A, B = generate.make_config_device(cfg, rp_dtype=torch.int64 if cfg == 5 else torch.int32)
+    else:
+        A = B = None
+    if world > 1:
+        same = (A is B) if rank == 0 else None
+        flag = torch.tensor([1 if same else 0], device=device)
+        dist.broadcast(flag, 0)
+        A = broadcast_csr(A, 0, device)
+        B = A if int(flag) else broadcast_csr(B, 0, device)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    sysp = detect_device_params()
+    stats = row_intermediate_stats(A, B)
+    inter = stats.inter_size
+    cuts, total_inter = flop_split(inter, world)
+    lo, hi = cuts[rank], cuts[rank + 1]
+    A_loc = row_block(A, lo, hi) if world > 1 else A
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)   # > 126 MB L2
+
+    def step(profile=False):
+        plan = MagnusPlan(A_loc, B, sys=sysp)
+        if profile:
+            plan.ctx.profile(True)
+        rp = plan.symbolic()
+        C, counters = plan.numeric(rp)
+        launches = plan.launches()
+        prof = plan.ctx.profile_read() if profile else None
+        plan.close()
+        return C, counters, launches, prof
+
+    for _ in range(args.warmup):
+        C, counters, _, _ = step()
+        del C
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    times, launches = [], 0
+    stream = torch.cuda.current_stream()
+    for _ in range(args.steps):
+        flush.zero_()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        C, counters, nl, _ = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+        launches += nl
+        del C
+    clocks = sampler.stop()
+    total_ms = sum(times)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t)
+    ms_step = total_ms / args.steps
+    gflops = 2.0 * total_inter / (ms_step * 1e-3) / 1e9
+
+    # kernel-level profile (one extra step, events bracket each launch on its stream)
+    C, counters, _, prof = step(profile=True)
+    c_nnz_row = (C.row_ptr[1:] - C.row_ptr[:-1])
+    nnz_c_local = int(C.row_ptr[-1])
+    rp_a = A_loc.row_ptr.element_size()
+    inter_loc = inter[lo:hi]
+    ab = algorithmic_bytes(A_loc, B, inter_loc, c_nnz_row, rp_a, B.row_ptr.element_size())
+    del C
+    peak, peak_kind = hbm_peak()
+    kern_bytes = {"num_heavy": ab["heavy"]["num_bytes"], "sym_heavy": ab["heavy"]["sym_bytes"],
+                  "num_block": ab["block"]["num_bytes"], "sym_block": ab["block"]["sym_bytes"],
+                  "num_warp": ab["warp"]["num_bytes"], "sym_warp": ab["warp"]["sym_bytes"]}
+    dom = max(prof, key=lambda k: prof[k][0])
+    dom_ms = prof[dom][0] / max(prof[dom][1], 1)
+    dom_bytes = kern_bytes.get(dom)
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_bytes else None
+    prof_share = {k: round(v[0], 3) for k, v in prof.items() if v[1]}
+
+    # whole-job compulsory roofline
+    nnz_c = nnz_c_local
+    if world > 1:
+        t = torch.tensor([nnz_c], dtype=torch.int64, device=device)
+        dist.all_reduce(t)
+        nnz_c = int(t)
+    comp = compulsory_bytes(A.n_rows, A.col.numel(), total_inter, nnz_c, A.row_ptr.element_size(),
+                            B.row_ptr.element_size(), 8, A.n_rows)
+
+    # e2e: host buffers through the public API (H2D of A, B + D2H of C inside the timed region)
+    e2e = None
+    if not args.no_e2e and rank == 0 and world == 1:
+        e2e = run_e2e(A, B, sysp, args.e2e_steps or max(1, min(args.steps, 3)), total_inter)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        A_h = A.numpy() if hasattr(A, "numpy") else A
+        B_h = A_h if B is A else B.numpy()
+        cpu = cpu_baseline(A_h, B_h, sysp, args.cpu_seconds, inter.cpu().numpy())
+
+    if rank == 0:
+        line = {
+            "metric": "SpGEMM GFLOP/s (2 x mults)",
+            "value": round(gflops, 3),
+            "unit": "GFLOP/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded, generated on device; BASELINE.json config shapes and value distributions)",
+            "config": {"workload": name, "n": A.n_rows, "nnz_a": int(A.col.numel()), "inter_products": total_inter,
+                       "nnz_c": nnz_c, "gflop": 2 * total_inter / 1e9, "l2": "flushed (256 MB write) before each step",
+                       "parallelism": f"rows split by flop over {world} GPU(s), B broadcast", "system_params": vars(sysp)
+                       if hasattr(sysp, "__dict__") else str(sysp)},
+            "hbm_gbs_compulsory": round(comp / (ms_step * 1e-3) / 1e9, 1),
+            "roofline_step": {"bound": "hbm", "compulsory_bytes": comp,
+                              "achieved": round(comp / (ms_step * 1e-3) / 1e9, 1), "peak": peak * world,
+                              "frac": round(comp / (ms_step * 1e-3) / 1e9 / (peak * world), 4), "unit": "GB/s"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1) if achieved else None,
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
+                         "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4)},
+            "kernel_ms": prof_share,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "gen_s": round(t_gen, 2),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(A, B, sysp, steps, total_inter):
+    """Same metric through spgemm_magnus with HOST inputs (pinned) and HOST outputs."""
+    import torch
+
+    from paper_2501_07056_b200 import CsrMatrix, MagnusPlan
+
+    def pinned(t):
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        return h
+
+    Ah = CsrMatrix(A.n_rows, A.n_cols, pinned(A.row_ptr), pinned(A.col), pinned(A.val))
+    Bh = Ah if B is A else CsrMatrix(B.n_rows, B.n_cols, pinned(B.row_ptr), pinned(B.col), pinned(B.val))
+    h2d = sum(t.numel() * t.element_size() for t in (Ah.row_ptr, Ah.col, Ah.val))
+    if Bh is not Ah:
+        h2d += sum(t.numel() * t.element_size() for t in (Bh.row_ptr, Bh.col, Bh.val))
+    out = {}
+    times = []
+    d2h = 0
+    for it in range(steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan = MagnusPlan(Ah, Bh, sys=sysp)           # H2D inside
+        rp = plan.symbolic()
+        C, _ = plan.numeric(rp)
+        nnz = int(rp[-1])
+        if "col" not in out or out["col"].numel() < nnz:
+            out = {"rp": torch.empty(A.n_rows + 1, dtype=torch.int64, pin_memory=True),
+                   "col": torch.empty(nnz, dtype=torch.int32, pin_memory=True),
+                   "val": torch.empty(nnz, dtype=torch.float64, pin_memory=True)}
+            if it == 0:
+                plan.close()
+                del C
+                continue  # first iteration only sizes the pinned output buffers
+        out["rp"].copy_(C.row_ptr, non_blocking=True)
+        out["col"][:nnz].copy_(C.col, non_blocking=True)
+        out["val"][:nnz].copy_(C.val, non_blocking=True)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+        d2h = (A.n_rows + 1) * 8 + nnz * 12
+        plan.close()
+        del C
+    t = sum(times) / len(times)
+    return {"value": round(2.0 * total_inter / t / 1e9, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(t * 1e3, 2), "steps": len(times)}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference algorithm's CPU restatement (oracle/) with all host
+    threads, on bounded row samples of the same workload (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_2501_07056_b200 import b200_default_params, generate
+    from paper_2501_07056_b200.generate import CONFIGS
+    name, p = config_desc(args.config)
+    t = time.perf_counter()
+    if args.config == 5:
+        print(json.dumps({"impl": "reference", "unavailable": "cfg5 host generation exceeds the bench budget"}))
+        return
+    try:
+        import torch
+        if torch.cuda.is_available():
+            from paper_2501_07056_b200 import _lib
+            _lib.build()
+            A, B = generate.make_config_device(args.config)
+            A = A.numpy()
+            B = A if CONFIGS[args.config]["product"] == "AA" else B.numpy()
+        else:
+            raise RuntimeError
+    except Exception:
+        A, B = generate.make_config_cpu(args.config)
+    rp = np.asarray(A.row_ptr, np.int64)
+    deg = np.diff(np.asarray(B.row_ptr, np.int64))
+    per = deg[np.asarray(A.col).astype(np.int64)]
+    cs = np.r_[0, np.cumsum(per)]
+    inter = cs[rp[1:]] - cs[rp[:-1]]
+    sysp = b200_default_params()
+    seconds = max(5.0, min(args.cpu_seconds, 30.0))
+    vals = []
+    for s in range(max(1, args.warmup // 3) + args.steps):
+        r = cpu_baseline(A, B, sysp, seconds / max(args.steps, 1) * 2, inter, seed=s)
+        if s >= max(1, args.warmup // 3):
+            vals.append(r)
+    v = float(np.mean([r["value"] for r in vals]))
+    line = {"impl": "reference", "metric": "SpGEMM GFLOP/s (2 x mults)", "value": round(v, 5), "unit": "GFLOP/s",
+            "n_gpus": world, "steps": len(vals), "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name},
+            "cpu_baseline": {"value": round(v, 5), "unit": "GFLOP/s", "cores": vals[0]["cores"], "kind": "port",
+                             "sample": vals[-1]["sample"]},
+            "e2e": {"value": round(v, 5), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": round(time.perf_counter() - t, 1)}
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

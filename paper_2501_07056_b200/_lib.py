@@ -28,14 +28,15 @@ def sources():
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile csrc/*.cu into libmagnus_b200.so (sm_100a).  No GPU needed."""
     srcs = sources()
-    hdr = os.path.join(ROOT, "include", "magnus_b200.h")
-    newest = max(os.path.getmtime(p) for p in srcs + [hdr])
+    hdrs = [os.path.join(ROOT, "include", h) for h in ("magnus_b200.h", "magnus_gen.h")]
+    newest = max(os.path.getmtime(p) for p in srcs + hdrs)
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
         return LIB_PATH
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     if not os.path.exists(nvcc):
         nvcc = "nvcc"
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB_PATH + ".tmp", os.path.join(CSRC, "magnus_b200.cu")]
+    cus = [p for p in srcs if p.endswith(".cu")]
+    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB_PATH + ".tmp", *cus]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
@@ -71,7 +72,10 @@ class Counters(C.Structure):
 # every symbol include/magnus_b200.h declares
 EXPORTS = ["magnus_compute_chunk_plan", "magnus_ctx_create", "magnus_ctx_destroy", "magnus_setup", "magnus_symbolic",
            "magnus_numeric", "magnus_row_stats", "magnus_categories", "magnus_launch_count", "magnus_last_error",
-           "magnus_version"]
+           "magnus_version", "magnus_profile_enable", "magnus_profile_read"]
+KERNEL_NAMES = ["row_stats", "categorize", "sym_warp", "sym_block", "sym_heavy", "scan", "num_warp", "num_block",
+                "num_heavy"]
+GEN_EXPORTS = ["magnus_gen_rmat_keys", "magnus_gen_uniform_pm1", "magnus_gen_uniform_rows"]
 
 _LIB = None
 
@@ -95,6 +99,12 @@ def lib():
         L.magnus_numeric.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Counters), C.c_void_p]
         L.magnus_row_stats.argtypes = [C.POINTER(Csr), C.POINTER(Csr), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.magnus_categories.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.magnus_gen_rmat_keys.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_uint64, C.c_double, C.c_double,
+                                           C.c_double, C.c_void_p, C.c_void_p]
+        L.magnus_gen_uniform_pm1.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p]
+        L.magnus_gen_uniform_rows.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_uint64, C.c_void_p, C.c_void_p]
+        L.magnus_profile_enable.argtypes = [C.c_void_p, C.c_int]
+        L.magnus_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.magnus_compute_chunk_plan.argtypes = [C.POINTER(Sys), C.c_int64, C.c_int, C.c_int, C.POINTER(Plan)]
         _LIB = L
     return _LIB
@@ -126,3 +136,14 @@ class Context:
 
     def launches(self) -> int:
         return int(lib().magnus_launch_count(self.h))
+
+    def profile(self, enable: bool = True) -> None:
+        check(lib().magnus_profile_enable(self.h, int(enable)))
+
+    def profile_read(self) -> dict:
+        """{kernel name: (total ms, launches)} since the last read (synchronises)."""
+        n = len(KERNEL_NAMES)
+        ms = (C.c_double * n)()
+        cnt = (C.c_int64 * n)()
+        check(lib().magnus_profile_read(self.h, ms, cnt))
+        return {KERNEL_NAMES[k]: (float(ms[k]), int(cnt[k])) for k in range(n)}

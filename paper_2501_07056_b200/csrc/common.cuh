@@ -51,7 +51,7 @@ __device__ __forceinline__ double pw_leaf(const F& x, int64_t off, int64_t n) {
 }
 
 template <class F>
-__device__ double pairwise(const F& x, int64_t off, int64_t n) {
+__device__ __noinline__ double pairwise(const F& x, int64_t off, int64_t n) {
   if (n <= 128) return pw_leaf(x, off, n);
   // explicit post-order traversal of numpy's recursion (split at n/2 rounded down to a multiple of 8)
   int64_t so[40], sn[40];

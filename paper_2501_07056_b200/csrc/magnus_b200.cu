@@ -102,6 +102,31 @@ struct magnus_ctx {
   int64_t host_stats[mg::kStatLen] = {0};
   int64_t coarse_batches = 0;
   mg::Sem sem{};
+  // profiling telemetry
+  bool profile = false;
+  struct Mark { int kernel; cudaEvent_t a, b; };
+  std::vector<Mark> marks;
+  std::vector<cudaEvent_t> event_pool;
+
+  cudaEvent_t get_event() {
+    if (!event_pool.empty()) { cudaEvent_t e = event_pool.back(); event_pool.pop_back(); return e; }
+    cudaEvent_t e; cudaEventCreate(&e); return e;
+  }
+  // bracket one launch: call begin() before and end() after
+  int pending = -1; cudaEvent_t pend_a = nullptr;
+  void begin(int kernel) {
+    ++launches;
+    if (!profile) return;
+    pend_a = get_event(); pending = kernel;
+    cudaEventRecord(pend_a, stream);
+  }
+  void end() {
+    if (!profile || pending < 0) return;
+    cudaEvent_t b = get_event();
+    cudaEventRecord(b, stream);
+    marks.push_back({pending, pend_a, b});
+    pending = -1;
+  }
 
   void free_all() {
     for (void* p : allocs) cudaFreeAsync(p, stream);
@@ -122,6 +147,28 @@ extern "C" {
 const char* magnus_last_error(void) { return g_err.c_str(); }
 const char* magnus_version(void) { return "magnus_b200 0.1 (sm_100a)"; }
 int64_t magnus_launch_count(magnus_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int magnus_profile_enable(magnus_ctx* ctx, int enable) {
+  if (!ctx) return set_err(MAGNUS_INPUT, "null argument");
+  ctx->profile = enable != 0;
+  return MAGNUS_OK;
+}
+
+int magnus_profile_read(magnus_ctx* ctx, double* ms, int64_t* launches) {
+  if (!ctx || !ms || !launches) return set_err(MAGNUS_INPUT, "null argument");
+  for (int k = 0; k < MAGNUS_K_COUNT; ++k) { ms[k] = 0.0; launches[k] = 0; }
+  for (auto& m : ctx->marks) {
+    MG_CUDA(cudaEventSynchronize(m.b));
+    float t = 0.f;
+    MG_CUDA(cudaEventElapsedTime(&t, m.a, m.b));
+    ms[m.kernel] += t;
+    launches[m.kernel] += 1;
+    ctx->event_pool.push_back(m.a);
+    ctx->event_pool.push_back(m.b);
+  }
+  ctx->marks.clear();
+  return MAGNUS_OK;
+}
 
 // compute_chunk_plan planner.py:106-152
 int magnus_compute_chunk_plan(const magnus_sys* sys, int64_t m_c, int numeric, int allow_coarse, magnus_chunk_plan* out) {
@@ -182,6 +229,8 @@ void magnus_ctx_destroy(magnus_ctx* ctx) {
   if (!ctx) return;
   ctx->free_all();
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto& m : ctx->marks) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
   delete ctx;
 }
 
@@ -245,15 +294,17 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   MG_CUDA(cudaMemsetAsync(ctx->stats, 0, mg::kStatLen * 8, s));
   MG_CUDA(cudaMemsetAsync(ctx->err, 0, 16, s));
   if (n > 0) {
+    ctx->begin(MAGNUS_K_ROW_STATS);
     rc = magnus_row_stats(A, B, ctx->inter, ctx->mn, ctx->mx, stream);
+    ctx->end();
     if (rc) return rc;
-    ++ctx->launches;
     mg::CatParams cp{th->sort_dense_crossover, sys->l2_bytes, sys->val_bytes, (int32_t)ctx->plan_sym.use_coarse};
     const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sm_count * 16);
+    ctx->begin(MAGNUS_K_CATEGORIZE);
     mg::k_categorize<<<grid, 256, 0, s>>>(n, ctx->A, ctx->inter, ctx->mn, ctx->mx, cp, ctx->cat, ctx->listW, ctx->listB,
                                           ctx->listH, ctx->listCoarse, ctx->stats);
+    ctx->end();
     MG_CUDA(cudaGetLastError());
-    ++ctx->launches;
   }
   unsigned long long hs[mg::kStatLen];
   MG_CUDA(cudaMemcpyAsync(hs, ctx->stats, sizeof hs, cudaMemcpyDeviceToHost, s));
@@ -305,8 +356,8 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   const int64_t nH = ctx->host_stats[mg::kStatNH];
   MG_CUDA(ctx->alloc(&ctx->modebits, std::max<int64_t>(1, nH) * ctx->sem.mode_words));
   const int64_t maxnk = ctx->host_stats[mg::kStatMaxNk];
-  ctx->gk_stride = maxnk > mg::kKS ? ((maxnk + 8) / 4) * 4 : 4;
-  MG_CUDA(ctx->alloc(&ctx->gk, (size_t)ctx->sm_count * ctx->gk_stride * 6));
+  ctx->gk_stride = maxnk > mg::kKSN ? ((maxnk + 8) / 4) * 4 : 4;
+  MG_CUDA(ctx->alloc(&ctx->gk, (size_t)2 * ctx->sm_count * ctx->gk_stride * 6));
   const bool chunk_global = n_chunks_global > mg::kChunkSmem;
   MG_CUDA(ctx->alloc(&ctx->gchunk, chunk_global ? (size_t)ctx->sm_count * n_chunks_global : 1));
   if (chunk_global) MG_CUDA(cudaMemsetAsync(ctx->gchunk, 0, (size_t)ctx->sm_count * n_chunks_global * 4, s));
@@ -327,40 +378,43 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
   const int64_t nW = ctx->host_stats[mg::kStatNW], nB = ctx->host_stats[mg::kStatNB], nH = ctx->host_stats[mg::kStatNH];
   if (nH > 0) {
     MG_CUDA(cudaMemsetAsync(ctx->work, 0, 8, s));
-    const unsigned grid = (unsigned)std::min<int64_t>(nH, ctx->sm_count);
+    const unsigned grid = (unsigned)std::min<int64_t>(nH, numeric ? 2 * ctx->sm_count : ctx->sm_count);
+    ctx->begin(numeric ? MAGNUS_K_NUM_HEAVY : MAGNUS_K_SYM_HEAVY);
     if (numeric)
-      mg::k_heavy_numeric<<<grid, mg::kHT, mg::HeavyNumSmem::kTotal, s>>>(
+      mg::k_heavy_numeric<<<grid, mg::kNT, mg::HeavyNumSmem::kTotal, s>>>(
           ctx->A, ctx->B, ctx->listH, nH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->modebits, c_rp, c_col, c_val, ctx->gk,
           ctx->gk_stride, ctx->work, ctx->err);
     else
       mg::k_heavy_symbolic<<<grid, mg::kHT, mg::HeavySymSmem::kTotal, s>>>(
           ctx->A, ctx->B, ctx->listH, nH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->counts, ctx->modebits, ctx->gk,
           ctx->gk_stride, ctx->gchunk, ctx->work);
+    ctx->end();
     MG_CUDA(cudaGetLastError());
-    ++ctx->launches;
   }
   if (nB > 0) {
     const unsigned grid = (unsigned)std::min<int64_t>(nB, (int64_t)ctx->sm_count * 3);
+    ctx->begin(numeric ? MAGNUS_K_NUM_BLOCK : MAGNUS_K_SYM_BLOCK);
     if (numeric)
       mg::k_rows_block<true><<<grid, mg::kBT, mg::kBSmem, s>>>(ctx->A, ctx->B, ctx->listB, nB, ctx->cat, ctx->sem,
                                                                 ctx->counts, c_rp, c_col, c_val, ctx->err);
     else
       mg::k_rows_block<false><<<grid, mg::kBT, mg::kBSmem, s>>>(ctx->A, ctx->B, ctx->listB, nB, ctx->cat, ctx->sem,
                                                                  ctx->counts, c_rp, c_col, c_val, ctx->err);
+    ctx->end();
     MG_CUDA(cudaGetLastError());
-    ++ctx->launches;
   }
   if (nW > 0) {
     const int64_t blocks = (nW + mg::kWT / 32 - 1) / (mg::kWT / 32);
     const unsigned grid = (unsigned)std::min<int64_t>(blocks, (int64_t)ctx->sm_count * 8);
+    ctx->begin(numeric ? MAGNUS_K_NUM_WARP : MAGNUS_K_SYM_WARP);
     if (numeric)
       mg::k_rows_warp<true><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts, c_rp,
                                                       c_col, c_val, ctx->err);
     else
       mg::k_rows_warp<false><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts,
                                                        c_rp, c_col, c_val, ctx->err);
+    ctx->end();
     MG_CUDA(cudaGetLastError());
-    ++ctx->launches;
   }
   return MAGNUS_OK;
 }
@@ -381,11 +435,13 @@ int magnus_symbolic(magnus_ctx* ctx, int64_t* c_row_ptr, int64_t* nnz_out, void*
   if (rc) return rc;
   // row_ptr = cumsum(counts)  (magnus.py:454-456)
   const int64_t tiles = (n + mg::kScanTile - 1) / mg::kScanTile;
+  ctx->begin(MAGNUS_K_SCAN);
   mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->counts, n, ctx->tile_sums);
   mg::k_scan_tiles<<<1, 1024, 0, s>>>(ctx->tile_sums, tiles);
   mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->counts, n, ctx->tile_sums, c_row_ptr);
+  ctx->end();
+  ctx->launches += 2;
   MG_CUDA(cudaGetLastError());
-  ctx->launches += 3;
   int64_t nnz = 0;
   MG_CUDA(cudaMemcpyAsync(&nnz, c_row_ptr + n, 8, cudaMemcpyDeviceToHost, s));
   MG_CUDA(cudaStreamSynchronize(s));
@@ -419,6 +475,23 @@ int magnus_numeric(magnus_ctx* ctx, const int64_t* c_row_ptr, uint32_t* c_col, d
     counters->rows_fine = ctx->host_stats[mg::kStatCat + 2];
     counters->rows_coarse = ctx->host_stats[mg::kStatCat + 3];
   }
+  return MAGNUS_OK;
+}
+
+// internal debug hook (not part of the public header): phase cycle counters of
+// k_heavy_numeric when built with -DMG_PROFILE_PHASES, else zeros.
+int magnus_debug_phases(unsigned long long* out16, int reset) {
+#ifdef MG_PROFILE_PHASES
+  MG_CUDA(cudaDeviceSynchronize());
+  MG_CUDA(cudaMemcpyFromSymbol(out16, mg::g_phase, 16 * 8));
+  if (reset) {
+    unsigned long long z[32] = {0};
+    MG_CUDA(cudaMemcpyToSymbol(mg::g_phase, z, sizeof z));
+  }
+#else
+  for (int i = 0; i < 16; ++i) out16[i] = 0;
+  (void)reset;
+#endif
   return MAGNUS_OK;
 }
 

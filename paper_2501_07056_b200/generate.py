@@ -157,3 +157,86 @@ def make_config_cpu(cfg: int):
         A = rmat(p["scale"], p["ef"], p["seed"])
         B = A
     return A, B
+
+
+# ------------------------------------------------------------------ device path
+def _gen_lib():
+    from . import _lib
+    return _lib.lib()
+
+
+def _seed_key(seed: int) -> int:
+    return int(seed) & 0xFFFFFFFFFFFFFFFF
+
+
+def rmat_device(scale: int, edge_factor: int, seed: int, a=0.57, b=0.19, c=0.19, device="cuda", rp_dtype=None):
+    """Same matrix as `rmat` (bit-identical), built on the GPU; returns a CsrMatrix of CUDA tensors."""
+    import ctypes as C
+
+    import torch
+
+    L = _gen_lib()
+    n = 1 << scale
+    m = edge_factor * n
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    keys = torch.empty(m, dtype=torch.int64, device=device)
+    step = 1 << 28
+    for lo in range(0, m, step):
+        cnt = min(step, m - lo)
+        rc = L.magnus_gen_rmat_keys(scale, lo, cnt, _seed_key(seed), a, b, c, C.c_void_p(keys.data_ptr() + lo * 8), stream)
+        assert rc == 0
+    keys = torch.unique(keys, sorted=True)          # merge duplicates (self-loops kept)
+    rows = keys >> scale
+    col = (keys & (n - 1)).to(torch.int32)
+    del keys
+    counts = torch.bincount(rows, minlength=n)
+    del rows
+    rp = torch.zeros(n + 1, dtype=torch.int64, device=device)
+    torch.cumsum(counts, 0, out=rp[1:])
+    if rp_dtype is not None:
+        rp = rp.to(rp_dtype)
+    val = torch.empty(col.numel(), dtype=torch.float64, device=device)
+    assert L.magnus_gen_uniform_pm1(_seed_key(seed), STREAM_VAL, col.numel(), C.c_void_p(val.data_ptr()), stream) == 0
+    return CsrMatrix(n, n, rp, col, val)
+
+
+def uniform_rows_device(n_rows: int, n_cols: int, d: int, seed: int, device="cuda", rp_dtype=None):
+    """Same matrix as `uniform_rows`, built on the GPU."""
+    import ctypes as C
+
+    import torch
+
+    L = _gen_lib()
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    col = torch.empty(n_rows * d, dtype=torch.int32, device=device)
+    assert L.magnus_gen_uniform_rows(n_rows, n_cols, d, _seed_key(seed), C.c_void_p(col.data_ptr()), stream) == 0
+    rp = torch.arange(n_rows + 1, dtype=torch.int64, device=device) * d
+    if rp_dtype is not None:
+        rp = rp.to(rp_dtype)
+    val = torch.empty(n_rows * d, dtype=torch.float64, device=device)
+    assert L.magnus_gen_uniform_pm1(_seed_key(seed), STREAM_VAL, n_rows * d, C.c_void_p(val.data_ptr()), stream) == 0
+    return CsrMatrix(n_rows, n_cols, rp, col, val)
+
+
+def stencil27_device(g: int, device="cuda", rp_dtype=None):
+    import torch
+    m = stencil27(g)
+    rp = torch.from_numpy(m.row_ptr).to(device)
+    if rp_dtype is not None:
+        rp = rp.to(rp_dtype)
+    return CsrMatrix(m.n_rows, m.n_cols, rp, torch.from_numpy(m.col).to(device), torch.from_numpy(m.val).to(device))
+
+
+def make_config_device(cfg: int, rp_dtype=None):
+    """(A, B) of a BASELINE config as CUDA tensors (cfg3: row_ptr int32 per BASELINE unless given)."""
+    p = CONFIGS[cfg]
+    if p["kind"] == "uniform":
+        A = uniform_rows_device(p["n"], p["n"], p["d"], p["seed"], rp_dtype=rp_dtype)
+        B = uniform_rows_device(p["n"], p["n"], p["d"], p["seed_b"], rp_dtype=rp_dtype) if p["product"] == "AB" else A
+    elif p["kind"] == "stencil":
+        A = stencil27_device(p["g"], rp_dtype=rp_dtype)
+        B = A
+    else:
+        A = rmat_device(p["scale"], p["ef"], p["seed"], rp_dtype=rp_dtype)
+        B = A
+    return A, B

@@ -16,7 +16,7 @@ from paper_2501_07056_b200 import _lib
 from paper_2501_07056_b200.accumulators import Accum
 from paper_2501_07056_b200.planner import NUMERIC, SYMBOLIC, fine_level_storage, max_l2_cols, round_pow2_of_sqrt
 
-HDR = os.path.join(os.path.dirname(__file__), "..", "include", "magnus_b200.h")
+HDRS = [os.path.join(os.path.dirname(__file__), "..", "include", h) for h in ("magnus_b200.h", "magnus_gen.h")]
 
 
 def test_planner_spec_examples():
@@ -82,7 +82,7 @@ def test_planner_optimality_and_oracle_agreement():
 
 def _header_symbols():
     import re
-    txt = open(HDR).read()
+    txt = "".join(open(h).read() for h in HDRS)
     return sorted(set(re.findall(r"^\s*(?:int|void|const char\*|int64_t|size_t)\s+(magnus_\w+)\s*\(", txt, re.M)))
 
 
@@ -90,7 +90,7 @@ def test_library_exports_every_header_symbol():
     _lib.build()
     L = _lib.lib()
     syms = _header_symbols()
-    assert set(syms) == set(_lib.EXPORTS)
+    assert set(syms) == set(_lib.EXPORTS) | set(_lib.GEN_EXPORTS)
     for s in syms:
         assert hasattr(L, s), s
     assert b"sm_100a" in L.magnus_version()
