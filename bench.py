@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=40.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -119,43 +119,6 @@ def config_desc(cfg):
              3: "cfg3 C=A.A R-MAT 2^20 ef16 (.57,.19,.19,.05)", 4: "cfg4 C=A.B uniform 2^23 8/row",
              5: "cfg5 C=A.A R-MAT 2^24 ef32"}
     return names[cfg], p
-
-
-def row_block(A, lo, hi):
-    """Rows [lo, hi) of a device CSR as a CSR view (row_ptr rebased)."""
-    from paper_2501_07056_b200 import CsrMatrix
-    rp = A.row_ptr
-    a0, a1 = int(rp[lo]), int(rp[hi])
-    return CsrMatrix(hi - lo, A.n_cols, (rp[lo:hi + 1] - a0).contiguous(), A.col[a0:a1], A.val[a0:a1])
-
-
-def flop_split(inter, world):
-    """Contiguous row cuts with ~equal sum(inter) per rank."""
-    import torch
-    cs = torch.cumsum(inter, 0)
-    total = int(cs[-1]) if cs.numel() else 0
-    cuts = [0]
-    for r in range(1, world):
-        cuts.append(int(torch.searchsorted(cs, torch.tensor(total * r // world, device=cs.device))))
-    cuts.append(int(inter.numel()))
-    return cuts, total
-
-
-def broadcast_csr(M, src, device):
-    import torch
-    import torch.distributed as dist
-    from paper_2501_07056_b200 import CsrMatrix
-    meta = torch.tensor([M.n_rows, M.n_cols, M.col.numel(), 1 if M.row_ptr.dtype == torch.int64 else 0]
-                        if M is not None else [0, 0, 0, 0], dtype=torch.int64, device=device)
-    dist.broadcast(meta, src)
-    n, m, nnz, rp64 = (int(x) for x in meta.tolist())
-    if M is None:
-        M = CsrMatrix(n, m, torch.empty(n + 1, dtype=torch.int64 if rp64 else torch.int32, device=device),
-                      torch.empty(nnz, dtype=torch.int32, device=device),
-                      torch.empty(nnz, dtype=torch.float64, device=device))
-    for t in (M.row_ptr, M.col, M.val):
-        dist.broadcast(t, src)
-    return M
 
 
 def algorithmic_bytes(A, B, inter, c_nnz_row, rp_bytes_a, rp_bytes_b):
@@ -238,6 +201,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2501_07056_b200 import MagnusPlan, _lib, detect_device_params, generate, row_intermediate_stats
+    from paper_2501_07056_b200.parallel import broadcast_csr, flop_cuts, row_block
 
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
@@ -390,48 +354,68 @@ def main():
         dist.destroy_process_group()
 
 
+class HostBuffer:
+    """Page-locked host array without the caching host allocator's power-of-two rounding
+    (C of cfg3 is ~117 GB): numpy memory registered with cudaHostRegister."""
+
+    def __init__(self, n, dtype):
+        import torch
+        self.arr = np.empty(max(int(n), 1), dtype=dtype)
+        self.rt = torch.cuda.cudart()
+        err = self.rt.cudaHostRegister(self.arr.ctypes.data, self.arr.nbytes, 0)
+        self.registered = int(err) == 0
+        self.t = torch.from_numpy(self.arr)
+
+    def close(self):
+        if self.registered:
+            self.rt.cudaHostUnregister(self.arr.ctypes.data)
+            self.registered = False
+
+
 def run_e2e(A, B, sysp, steps, total_inter):
-    """Same metric through spgemm_magnus with HOST inputs (pinned) and HOST outputs."""
+    """Same metric through the public API with HOST buffers: page-locked host inputs are copied
+    in, spgemm runs, and C (row_ptr, col, val) is read back into page-locked host arrays --
+    all inside the timed region (buffers are allocated and registered outside it)."""
     import torch
 
     from paper_2501_07056_b200 import CsrMatrix, MagnusPlan
 
-    def pinned(t):
-        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-        h.copy_(t)
+    def pinned_copy(t):
+        h = HostBuffer(t.numel(), {torch.int32: np.int32, torch.int64: np.int64, torch.float64: np.float64}[t.dtype])
+        h.t.copy_(t)
         return h
 
-    Ah = CsrMatrix(A.n_rows, A.n_cols, pinned(A.row_ptr), pinned(A.col), pinned(A.val))
-    Bh = Ah if B is A else CsrMatrix(B.n_rows, B.n_cols, pinned(B.row_ptr), pinned(B.col), pinned(B.val))
-    h2d = sum(t.numel() * t.element_size() for t in (Ah.row_ptr, Ah.col, Ah.val))
-    if Bh is not Ah:
-        h2d += sum(t.numel() * t.element_size() for t in (Bh.row_ptr, Bh.col, Bh.val))
-    out = {}
+    bufs = [pinned_copy(t) for t in (A.row_ptr, A.col, A.val)]
+    Ah = CsrMatrix(A.n_rows, A.n_cols, bufs[0].t, bufs[1].t, bufs[2].t)
+    Bh = Ah
+    if B is not A:
+        bufs += [pinned_copy(t) for t in (B.row_ptr, B.col, B.val)]
+        Bh = CsrMatrix(B.n_rows, B.n_cols, bufs[3].t, bufs[4].t, bufs[5].t)
+    h2d = sum(b.arr.nbytes for b in bufs)
+    # size the output once (symbolic only), outside the timed region
+    plan = MagnusPlan(A, B, sys=sysp)
+    rp = plan.symbolic()
+    nnz = int(rp[-1])
+    plan.close()
+    del rp
+    out_rp, out_col, out_val = HostBuffer(A.n_rows + 1, np.int64), HostBuffer(nnz, np.int32), HostBuffer(nnz, np.float64)
     times = []
-    d2h = 0
-    for it in range(steps + 1):
+    for _ in range(steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        plan = MagnusPlan(Ah, Bh, sys=sysp)           # H2D inside
+        plan = MagnusPlan(Ah, Bh, sys=sysp)           # H2D of the host inputs inside
         rp = plan.symbolic()
         C, _ = plan.numeric(rp)
-        nnz = int(rp[-1])
-        if "col" not in out or out["col"].numel() < nnz:
-            out = {"rp": torch.empty(A.n_rows + 1, dtype=torch.int64, pin_memory=True),
-                   "col": torch.empty(nnz, dtype=torch.int32, pin_memory=True),
-                   "val": torch.empty(nnz, dtype=torch.float64, pin_memory=True)}
-            if it == 0:
-                plan.close()
-                del C
-                continue  # first iteration only sizes the pinned output buffers
-        out["rp"].copy_(C.row_ptr, non_blocking=True)
-        out["col"][:nnz].copy_(C.col, non_blocking=True)
-        out["val"][:nnz].copy_(C.val, non_blocking=True)
+        out_rp.t.copy_(C.row_ptr, non_blocking=True)
+        out_col.t[:nnz].copy_(C.col, non_blocking=True)
+        out_val.t[:nnz].copy_(C.val, non_blocking=True)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
-        d2h = (A.n_rows + 1) * 8 + nnz * 12
         plan.close()
-        del C
+        del C, rp
+    d2h = (A.n_rows + 1) * 8 + nnz * 12
+    for b in bufs + [out_rp, out_col, out_val]:
+        b.close()
     t = sum(times) / len(times)
     return {"value": round(2.0 * total_inter / t / 1e9, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(t * 1e3, 2), "steps": len(times)}

@@ -14,6 +14,7 @@ struct DevCsr {
   const int32_t* rp32;
   const uint32_t* col;
   const double* val;
+  const uint32_t* skip;   // skip[j] = col[32*j] (built for B by magnus_setup; gallops over long rows)
   __device__ __forceinline__ int64_t rp(int64_t i) const { return rp64 ? __ldg(rp64 + i) : (int64_t)__ldg(rp32 + i); }
 };
 

@@ -37,9 +37,10 @@ __device__ unsigned long long g_phase[32];
 #endif
 
 constexpr int kHT = 512;                // symbolic: threads per CTA (1 CTA / SM)
-constexpr int kNT = 256;                // numeric: threads per CTA (2 CTAs / SM)
-constexpr int kCap = 4096;              // numeric: stream elements per batch
+constexpr int kNT = 512;                // numeric: threads per CTA (1 CTA / SM)
+constexpr int kCap = 8192;              // numeric: stream elements per batch
 constexpr int kItems = kCap / kNT;      // 16 stream elements per thread per batch
+constexpr int kSymItems = 16;           // symbolic: stream elements per thread per tile
 constexpr int kKS = 1024;               // symbolic: k's whose cursors live in shared memory
 constexpr int kKSN = 512;               // numeric: k's whose cursors live in shared memory
 constexpr int kSymWin = 1 << 20;        // symbolic window width (columns; 128 KB bitmap)
@@ -80,17 +81,29 @@ __device__ uint32_t block_scan_striped(uint32_t* a, int n, uint32_t* scratch) {
 }
 
 // first index in [lo, hi) with col[idx] >= key, galloping from lo (segment ends
-// are usually a few elements past the cursor)
-__device__ __forceinline__ uint32_t gallop_col(const uint32_t* __restrict__ col, uint32_t lo, uint32_t hi, uint32_t key) {
+// are usually a few elements past the cursor).  Long hops go over the skip list
+// (every 32nd column of B) so a hub row costs ~log2(distance/32) probes of a
+// dense index plus one 128-byte line, not log2(distance) scattered misses.
+__device__ __forceinline__ uint32_t gallop_col(const DevCsr& B, uint32_t lo, uint32_t hi, uint32_t key) {
+  const uint32_t* __restrict__ col = B.col;
   if (lo >= hi || __ldg(col + lo) >= key) return lo;
-  uint32_t step = 1, prev = lo;   // invariant: col[prev] < key
+  const uint32_t blk_end = (lo | 31u) + 1u;   // first block head after lo
+  if (blk_end >= hi || __ldg(B.skip + (blk_end >> 5)) >= key) return lower_bound_col(col, lo + 1, min(blk_end, hi), key);
+  uint32_t jlo = blk_end >> 5;                // col[32*jlo] < key
+  const uint32_t jmax = (hi - 1) >> 5;        // last block head inside [lo, hi)
+  uint32_t jhi = jmax + 1, step = 1;
   while (true) {
-    const uint32_t nxt = prev + step;
-    if (nxt >= hi) return lower_bound_col(col, prev + 1, hi, key);
-    if (__ldg(col + nxt) >= key) return lower_bound_col(col, prev + 1, nxt, key);
-    prev = nxt;
+    const uint32_t j = jlo + step;
+    if (j > jmax) break;
+    if (__ldg(B.skip + j) >= key) { jhi = j; break; }
+    jlo = j;
     step <<= 1;
   }
+  while (jhi - jlo > 1) {
+    const uint32_t mid = (jlo + jhi) >> 1;
+    if (__ldg(B.skip + mid) < key) jlo = mid; else jhi = mid;
+  }
+  return lower_bound_col(col, jlo * 32u + 1u, min(jhi * 32u, hi), key);
 }
 
 // Per-row k state: cursor (next B position in this row), segment end in the
@@ -120,7 +133,7 @@ __device__ __forceinline__ uint32_t kstate_segments(const KState& st, const DevC
                                                     uint32_t* scratch) {
   for (int t = threadIdx.x; t < nk; t += T) {
     const uint32_t s = st.ks[t], e0 = st.kend[t];
-    const uint32_t e = hi_all ? e0 : gallop_col(B.col, s, e0, hi);
+    const uint32_t e = hi_all ? e0 : gallop_col(B, s, e0, hi);
     st.ke[t] = e;
     st.koff[t] = e - s;
   }
@@ -226,11 +239,11 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
       const bool hi_all = hi > row_hi;
       const uint32_t S = kstate_segments<kHT>(st, B, nk, (uint32_t)(hi_all ? 0 : hi), hi_all, scratch);
       // stream elements: blocked assignment, one search per thread per tile
-      for (uint32_t t0 = 0; t0 < S; t0 += kHT * kItems) {
-        const uint32_t q0 = t0 + threadIdx.x * kItems;
+      for (uint32_t t0 = 0; t0 < S; t0 += kHT * kSymItems) {
+        const uint32_t q0 = t0 + threadIdx.x * kSymItems;
         if (q0 < S) {
           int t = kstate_find(st, nk, q0);
-          for (uint32_t q = q0; q < min(S, q0 + kItems); ++q) {
+          for (uint32_t q = q0; q < min(S, q0 + kSymItems); ++q) {
             while (st.koff[t + 1] <= q) ++t;
             const uint32_t pos = st.ks[t] + (q - st.koff[t]);
             const uint32_t c = __ldg(B.col + pos);
@@ -274,56 +287,32 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
 }
 
 // ------------------------------------------------------------------ numeric
-// Window machinery (per CTA, one row at a time):
-//  * a window [lo, lo+W) whose stream fits one batch (S <= kCap) is "wide"
-//    (W up to 2^18): its columns are compacted through a bitmap (rank = word
-//    prefix + popcount), so buckets are indexed by output rank and every phase
-//    costs O(S + W/32) -- sparse windows pay nothing per empty column;
-//  * a window that cannot fit one batch (dense hub regions) is "dense"
-//    (W <= 8192): its stream is processed in batches and every column keeps a
-//    carry in shared memory (sequential association only; windows containing
-//    pairwise columns are narrowed until they fit one batch).
-constexpr uint32_t kSmallBucket = 12;
+// Per CTA, one row at a time, window by window.  A window's stream (ascending
+// k) is staged in shared memory in batches of kCap elements and stably sorted
+// by column with a block-wide LSD radix sort (warp ballot ranking, per-warp
+// digit histograms): after the sort every column's contributions are one run
+// in ascending k, which is exactly the order the reference adds them in.
+//  * "wide" window (whole stream fits one batch, up to 2^17 columns): columns
+//    are first compacted to ranks through a bitmap (rank = word prefix +
+//    popcount), the sort key is the rank (< 8192, 13 bits, 2 passes) and each
+//    run is reduced straight to its output slot; pairwise columns allowed.
+//  * "dense" window (stream > kCap, <= 4096 columns, sequential association
+//    only -- windows holding pairwise columns are narrowed until they fit one
+//    batch): key = window-local column (12 bits), runs add into a per-column
+//    carry; the touched columns are emitted when the window is done.
 constexpr int kWinWide = 1 << 17;
 constexpr int kWinDense = 4096;
 constexpr int kWordsWide = kWinWide / 32;   // 4096
 constexpr int kWordsDense = kWinDense / 32; // 128
+constexpr int kRadixBits = 7;
+constexpr int kRadix = 1 << kRadixBits;     // 128 digits
+constexpr int kNW = kNT / 32;               // 16 warps
+constexpr int kWaves = kCap / kNT;          // 16 waves of 32 per warp
 
-__device__ __forceinline__ void insertion_sort_u16(uint16_t* bp, uint32_t s0, uint32_t e0) {
-  for (uint32_t a = s0 + 1; a < e0; ++a) {
-    const uint16_t kp = bp[a];
-    uint32_t b = a;
-    while (b > s0 && bp[b - 1] > kp) { bp[b] = bp[b - 1]; --b; }
-    bp[b] = kp;
-  }
-}
-
-// Order a big bucket (distinct stream positions) with one warp: mark the
-// positions in a per-warp bitmap over the batch, then write them back
-// ascending (ballot-free word prefix).  O(d + batch/32).
-__device__ __noinline__ void warp_order_bucket(uint16_t* bp, uint32_t s0, uint32_t e0, uint32_t* wbm, int nbw, int lane) {
-  for (uint32_t a = s0 + lane; a < e0; a += 32) {
-    const uint32_t q = bp[a];
-    atomicOr(&wbm[q >> 5], 1u << (q & 31));
-  }
-  __syncwarp();
-  uint32_t base = s0;
-  for (int w0 = 0; w0 < nbw; w0 += 32) {
-    const int wd = w0 + lane;
-    uint32_t bits = wd < nbw ? wbm[wd] : 0u;
-    const uint32_t cnt = __popc(bits);
-    const uint32_t inc = warp_incl_scan(cnt);
-    uint32_t o = base + inc - cnt;
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1u;
-      bp[o++] = (uint16_t)(wd * 32 + b);
-    }
-    if (wd < nbw) wbm[wd] = 0;
-    base += __shfl_sync(0xffffffffu, inc, 31);
-  }
-  __syncwarp();
-}
+// Staging layouts are written blocked (thread t owns positions 16t..16t+15) and read
+// lane-consecutive; one pad slot per 16 entries keeps both bank-conflict free.
+__device__ __forceinline__ uint32_t pad_v(uint32_t q) { return q + (q >> 4); }          // doubles
+__device__ __forceinline__ uint32_t pad_k(uint32_t q) { return q + ((q >> 4) << 1); }   // u16 pairs
 
 // true: the reference's dense accumulator (sequential from +0.0); false: its sort accumulator
 __device__ __forceinline__ bool column_seq(int ci, int64_t col, const Sem& sem, const uint32_t* __restrict__ mb) {
@@ -333,127 +322,114 @@ __device__ __forceinline__ bool column_seq(int ci, int64_t col, const Sem& sem, 
   return (__ldg(mb + (f >> 5)) >> (f & 31)) & 1u;
 }
 
-__device__ __noinline__ double bucket_pairwise(const double* sv, const uint16_t* bp, uint32_t s0, uint32_t e0) {
-  auto x = [&](int64_t q) { return sv[bp[q]]; };
-  double s = sv[bp[s0]];
+// Sequential (ascending-k) sum of a run: values sv[pay[a]] for a in [s0, e0).
+__device__ __forceinline__ double run_seq(const double* sv, const uint16_t* pay, uint32_t s0, uint32_t e0, double carry) {
+  double s = carry;
+  uint32_t a = s0;
+  for (; a + 8 <= e0; a += 8) {   // independent loads first, then the ordered chain
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = sv[pad_v(pay[a + u])];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+  }
+  for (; a < e0; ++a) s = __dadd_rn(s, sv[pad_v(pay[a])]);
+  return s;
+}
+
+__device__ __noinline__ double run_pairwise(const double* sv, const uint16_t* pay, uint32_t s0, uint32_t e0) {
+  auto x = [&](int64_t q) { return sv[pad_v(pay[q])]; };
+  double s = sv[pad_v(pay[s0])];
   if (e0 - s0 > 1) s = __dadd_rn(s, pairwise(x, s0 + 1, e0 - s0 - 1));
   return s;
 }
 
-// value of one column bucket (positions bp[s0..e0) ascending, values staged in sv[q])
-__device__ __forceinline__ double bucket_value(const double* sv, const uint16_t* bp, uint32_t s0, uint32_t e0, bool seq,
-                                               double carry) {
-  if (seq) {
-    double s = carry;
-    uint32_t a = s0;
-    for (; a + 8 <= e0; a += 8) {   // independent loads first, then the ordered chain
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = sv[bp[a + u]];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
-    }
-    for (; a < e0; ++a) s = __dadd_rn(s, sv[bp[a]]);
-    return s;
-  }
-  return bucket_pairwise(sv, bp, s0, e0);
-}
-
-// Visit every set column of the batch bitmap: the m columns are split evenly
-// over the warps by rank, and within a warp the set bits of each 32-word chunk
-// are dealt to the lanes in rounds of 32 (balanced even when hub regions make a
-// few words dense).  fn(c, r) gets the window-local column and its rank.
-template <class Fn>
-__device__ __forceinline__ void for_each_column(const uint32_t* bm, const uint32_t* wpref, int nwords, uint32_t m,
-                                                const Fn& fn) {
-  constexpr int NW = kNT / 32;
+// One stable LSD pass over n <= kCap (key, payload) pairs on digit (key >> shift) & (2^bits - 1).
+// Warp w owns the contiguous positions [w*per, (w+1)*per), per = ceil(n/kNW) rounded to
+// 32, walked in waves of 32 (stable: warps in order, waves in order, lanes in order).
+template <bool PaddedIn>
+__device__ __forceinline__ void radix_pass(const uint16_t* kin, const uint16_t* pin, uint16_t* kout, uint16_t* pout,
+                                           uint32_t n, int shift, int bits, uint32_t* hist, uint32_t* scratch) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const uint32_t r_lo = (uint32_t)(((uint64_t)m * wid) / NW), r_hi = (uint32_t)(((uint64_t)m * (wid + 1)) / NW);
-  if (r_lo >= r_hi) return;
-  int lo = 0, hi = nwords;   // last word with wpref <= r_lo (and a set bit at/after it)
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (wpref[mid] <= r_lo) lo = mid; else hi = mid;
-  }
-  for (int w0 = lo; w0 < nwords; w0 += 32) {
-    const int wd = w0 + lane;
-    const uint32_t bits = wd < nwords ? bm[wd] : 0u;
-    const uint32_t base = wd < nwords ? wpref[wd] : 0xffffffffu;
-    if (__shfl_sync(0xffffffffu, base, 0) >= r_hi) break;
-    const uint32_t cnt = __popc(bits);
-    const uint32_t inc = warp_incl_scan(cnt);
-    const uint32_t excl = inc - cnt;
-    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    for (uint32_t g0 = 0; g0 < total; g0 += 32) {
-      const uint32_t g = g0 + lane;
-      int src = 0;   // lane whose word holds the g-th set bit of the chunk
+  const uint32_t lt = (1u << lane) - 1u;
+  const int nd = 1 << bits;
+  const uint32_t per = ((n + kNW - 1) / kNW + 31) & ~31u;
+  const uint32_t base0 = (uint32_t)wid * per;
+  const int nwave = base0 >= n ? 0 : (int)((min(n - base0, per) + 31) / 32);
+  for (int i = threadIdx.x; i < nd * kNW; i += kNT) hist[i] = 0;
+  __syncthreads();
+  uint32_t info[kWaves];   // digit | rank-in-wave << 8 | run count << 16 ; 0xffffffff = empty lane
 #pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const uint32_t e = __shfl_sync(0xffffffffu, excl, src + step);
-        if (src + step < 32 && e <= g) src += step;
+  for (int wv = 0; wv < kWaves; ++wv) {
+    info[wv] = 0xffffffffu;
+    if (wv < nwave) {
+      const uint32_t i = base0 + wv * 32 + lane;
+      const bool valid = i < n;
+      const uint32_t d = valid ? ((uint32_t)kin[PaddedIn ? pad_k(i) : i] >> shift) & (uint32_t)(nd - 1) : 0u;
+      uint32_t peers = __ballot_sync(0xffffffffu, valid);
+      for (int b = 0; b < bits; ++b) {
+        const uint32_t m = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? m : ~m;
       }
-      const uint32_t sbits = __shfl_sync(0xffffffffu, bits, src);
-      const uint32_t sexcl = __shfl_sync(0xffffffffu, excl, src);
-      const uint32_t sbase = __shfl_sync(0xffffffffu, base, src);
-      if (g < total) {
-        const uint32_t nth = g - sexcl;
-        const uint32_t bit = __fns(sbits, 0, nth + 1);
-        const uint32_t r = sbase + nth;
-        if (r >= r_lo && r < r_hi) fn((uint32_t)((w0 + src) * 32 + bit), r);
-      }
+      const uint32_t rank = __popc(peers & lt);
+      if (valid && rank == 0) hist[d * kNW + wid] += __popc(peers);
+      if (valid) info[wv] = d | (rank << 8) | ((uint32_t)__popc(peers) << 16);
+      __syncwarp();   // next wave's leaders may update the same counter
     }
   }
+  __syncthreads();
+  block_scan_striped<kNT>(hist, nd * kNW, scratch);
+#pragma unroll
+  for (int wv = 0; wv < kWaves; ++wv) {
+    if (wv < nwave) {
+      const uint32_t f = info[wv];
+      const uint32_t i = base0 + wv * 32 + lane;
+      uint32_t base = 0;
+      if (f != 0xffffffffu) {
+        base = hist[(f & 0xffu) * kNW + wid];
+        const uint32_t pos = base + ((f >> 8) & 0xffu);
+        kout[pos] = kin[PaddedIn ? pad_k(i) : i];
+        pout[pos] = pin[PaddedIn ? pad_k(i) : i];
+      }
+      __syncwarp();
+      if (f != 0xffffffffu && ((f >> 8) & 0xffu) == 0u) hist[(f & 0xffu) * kNW + wid] = base + (f >> 16);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
 }
-
-constexpr int kBatchWords = kCap / 32;   // 128
 
 struct HeavyNumSmem {
-  static constexpr size_t kRegion = (size_t)kWordsWide * 4 * 2;   // 64 KB: wide bitmap+prefix | dense carry
-  static constexpr size_t kSmall = (size_t)kWordsDense * 4 * 3;   // dense: batch bitmap, prefix, touched
-  static constexpr size_t kCntl = (size_t)kCap * 4;                // 32 KB bucket counts / offsets
-  static constexpr size_t kSv = (size_t)kCap * 8;                  // 64 KB values by stream position
-  static constexpr size_t kBp = (size_t)kCap * 2;                  // 16 KB bucket entries (stream positions)
-  static constexpr size_t kWbm = (size_t)(kNT / 32) * kBatchWords * 4;  // 16 KB per-warp ordering bitmaps
+  static constexpr size_t kSv = (size_t)(kCap + kCap / 16) * 8;    // 68 KB values by (padded) stream position
+  static constexpr size_t kKeys = (size_t)(kCap + kCap / 8 + kCap) * 2;   // 34 KB sort keys: padded in | out
+  static constexpr size_t kPays = (size_t)(kCap + kCap / 8 + kCap) * 2;   // 34 KB payloads = stream positions
+  static constexpr size_t kRegion = (size_t)kWordsWide * 4 * 2;     // 32 KB wide bitmap+prefix | dense carry
+  static constexpr size_t kTb = (size_t)kWordsDense * 4 * 2;        // dense touched bitmap + prefix
+  static constexpr size_t kPw = (size_t)(kCap / 32) * 4;            // wide: pairwise flag per rank
+  static constexpr size_t kHist = (size_t)kRadix * kNW * 4;         // 8 KB
+  static constexpr size_t kKcnt = (size_t)kCap * 4;                 // 32 KB elements per sort key -> run starts
   static constexpr size_t kK = (size_t)kKSN * 4 * 4 + (kKSN + 4) * 4 + kKSN * 8;
-  static constexpr size_t kBig = ((kCap / kSmallBucket + 8) * 4 + 15) / 16 * 16;
   static constexpr size_t kScratch = 64 * 8;
-  static constexpr size_t kTotal = kRegion + kSmall + kCntl + kSv + kBp + kWbm + kK + kBig + kScratch;
-  static_assert(kRegion % 16 == 0 && kSmall % 16 == 0 && kCntl % 16 == 0 && kSv % 16 == 0 && kBp % 16 == 0 &&
-                    kWbm % 16 == 0 && kK % 16 == 0 && kBig % 16 == 0,
+  static constexpr size_t kTotal = kSv + kKeys + kPays + kRegion + kTb + kPw + kHist + kKcnt + kK + kScratch;
+  static_assert(kSv % 16 == 0 && kKeys % 16 == 0 && kPays % 16 == 0 && kRegion % 16 == 0 && kTb % 16 == 0 &&
+                    kPw % 16 == 0 && kHist % 16 == 0 && kK % 16 == 0,
                 "shared-memory sections must keep 16-byte alignment");
-  static_assert(kTotal <= 113 * 1024, "two CTAs per SM (228 KB shared memory per SM)");
+  static_assert(kTotal <= 232448, "fits the 227 KB opt-in shared memory of a B200 CTA");
 };
 
-struct NumCtx {
-  uint32_t* bm;     // bitmap of the batch's columns (wide: kWordsWide, dense: kWordsDense)
-  uint32_t* wpref;  // word prefix popcounts
-  uint32_t* cntl;   // bucket counts -> ends
-  double* sv;       // staged values, indexed by stream position in the batch
-  uint16_t* bp;     // bucket entries: stream positions
-  uint32_t* wbm;    // per-warp ordering bitmaps
-  uint32_t* big;
-  uint32_t* nbig;
-  uint32_t* scratch;
-};
-
-// Gather stream positions [B0 + q0, B0 + q0 + kItems) of the window: column into
-// registers (window-local), value into sv[q] (q = position in the batch).
-struct Items {
-  uint32_t c[kItems];   // window-local column, then its rank (bucket)
-  int n;
-};
-
-__device__ __forceinline__ void gather_items(const KState& st, const DevCsr& B, int nk, uint32_t B0, uint32_t nb,
-                                             int64_t lo, Items& it, double* sv) {
+// Stage stream positions [B0, B0 + nb) of the window: value into sv[q]; window-local
+// column returned in c[] (q = position in the batch = threadIdx.x * kItems + j).
+__device__ __forceinline__ int stage_items(const KState& st, const DevCsr& B, int nk, uint32_t B0, uint32_t nb, int64_t lo,
+                                           double* sv, uint32_t* c) {
   const uint32_t q0 = threadIdx.x * kItems;
-  it.n = q0 < nb ? (int)min((uint32_t)kItems, nb - q0) : 0;
+  const int n = q0 < nb ? (int)min((uint32_t)kItems, nb - q0) : 0;
   uint32_t pos[kItems];
   int tk[kItems];
-  if (it.n > 0) {
+  if (n > 0) {
     int t = kstate_find(st, nk, B0 + q0);
 #pragma unroll
     for (int j = 0; j < kItems; ++j) {
-      if (j < it.n) {
+      if (j < n) {
         const uint32_t p = B0 + q0 + j;
         while (st.koff[t + 1] <= p) ++t;
         pos[j] = st.ks[t] + (p - st.koff[t]);
@@ -463,62 +439,25 @@ __device__ __forceinline__ void gather_items(const KState& st, const DevCsr& B, 
   }
 #pragma unroll
   for (int j = 0; j < kItems; ++j)
-    if (j < it.n) it.c[j] = (uint32_t)((int64_t)__ldg(B.col + pos[j]) - lo);
+    if (j < n) c[j] = (uint32_t)((int64_t)__ldg(B.col + pos[j]) - lo);
 #pragma unroll
   for (int j = 0; j < kItems; ++j)
-    if (j < it.n) sv[q0 + j] = __dmul_rn(st.kav[tk[j]], __ldg(B.val + pos[j]));
+    if (j < n) sv[pad_v(q0 + j)] = __dmul_rn(st.kav[tk[j]], __ldg(B.val + pos[j]));
+  return n;
 }
 
-// One batch through the bucket pipeline: mark -> rank -> count -> scan -> scatter.
-// Returns m = distinct columns of the batch; afterwards bucket r holds the
-// stream positions bp[(r ? cntl[r-1] : 0) .. cntl[r]) (unordered) and bm/wpref
-// describe the columns.
-__device__ __forceinline__ uint32_t bucket_batch(const NumCtx& x, Items& it, int nwords) {
-#pragma unroll
-  for (int j = 0; j < kItems; ++j)
-    if (j < it.n) atomicOr(&x.bm[it.c[j] >> 5], 1u << (it.c[j] & 31));
-  __syncthreads();
-  for (int w = threadIdx.x; w < nwords; w += kNT) x.wpref[w] = __popc(x.bm[w]);
-  __syncthreads();
-  const uint32_t m = block_scan_striped<kNT>(x.wpref, nwords, x.scratch);
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    if (j < it.n) {
-      const uint32_t w = it.c[j] >> 5, bit = 1u << (it.c[j] & 31);
-      it.c[j] = x.wpref[w] + __popc(x.bm[w] & (bit - 1u));
-      atomicAdd(&x.cntl[it.c[j]], 1u);
-    }
-  }
-  __syncthreads();
-  block_scan_striped<kNT>(x.cntl, (int)m, x.scratch);
-  const uint32_t q0 = threadIdx.x * kItems;
-#pragma unroll
-  for (int j = 0; j < kItems; ++j) {
-    if (j < it.n) {
-      const uint32_t slot = atomicAdd(&x.cntl[it.c[j]], 1u);
-      x.bp[slot] = (uint16_t)(q0 + j);
-    }
-  }
-  __syncthreads();
-  return m;
-}
-
-// Big buckets (hub columns): one warp each puts the bucket into stream order,
-// then lane 0 runs the ordered sum; finish(c, r, s0, e0) is called by lane 0.
-template <class Finish>
-__device__ __forceinline__ void big_buckets(const NumCtx& x, uint32_t nb, const Finish& finish) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nbw = (int)((nb + 31) >> 5);
-  for (uint32_t b = wid; b < *x.nbig; b += kNT / 32) {
-    const uint32_t c = x.big[b] >> 13, r = x.big[b] & 8191u;
-    const uint32_t s0 = r ? x.cntl[r - 1] : 0u, e0 = x.cntl[r];
-    warp_order_bucket(x.bp, s0, e0, x.wbm + wid * kBatchWords, nbw, lane);
-    if (lane == 0) finish(c, r, s0, e0);
-    __syncwarp();
+// After the sort, key k's run is [kcnt[k-1], kcnt[k]) (kcnt = inclusive prefix of the
+// per-key element counts).  fn(k, s0, e0) for every key with a non-empty run; keys are
+// dealt to threads round-robin.
+template <class Fn>
+__device__ __forceinline__ void for_each_key(const uint32_t* kcnt, uint32_t nkeys, const Fn& fn) {
+  for (uint32_t k = threadIdx.x; k < nkeys; k += kNT) {
+    const uint32_t s0 = k ? kcnt[k - 1] : 0u, e0 = kcnt[k];
+    if (e0 > s0) fn(k, s0, e0);
   }
 }
 
-__global__ void __launch_bounds__(kNT, 2)
+__global__ void __launch_bounds__(kNT, 1)
 k_heavy_numeric(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows, const int8_t* __restrict__ cat,
                 const int64_t* __restrict__ mn, const int64_t* __restrict__ mx, Sem sem,
                 const uint32_t* __restrict__ modebits, const int64_t* __restrict__ c_rp, uint32_t* __restrict__ c_col,
@@ -526,31 +465,29 @@ k_heavy_numeric(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nr
                 unsigned long long* __restrict__ work, unsigned long long* __restrict__ err) {
   extern __shared__ __align__(16) unsigned char smem[];
   unsigned char* sp = smem;
-  NumCtx x;
+  double* sv = reinterpret_cast<double*>(sp); sp += HeavyNumSmem::kSv;
+  uint16_t* key0 = reinterpret_cast<uint16_t*>(sp);
+  uint16_t* key1 = key0 + kCap + kCap / 8; sp += HeavyNumSmem::kKeys;
+  uint16_t* pay0 = reinterpret_cast<uint16_t*>(sp);
+  uint16_t* pay1 = pay0 + kCap + kCap / 8; sp += HeavyNumSmem::kPays;
   unsigned char* region = sp; sp += HeavyNumSmem::kRegion;
-  uint32_t* small = reinterpret_cast<uint32_t*>(sp); sp += HeavyNumSmem::kSmall;
-  x.cntl = reinterpret_cast<uint32_t*>(sp); sp += HeavyNumSmem::kCntl;
-  x.sv = reinterpret_cast<double*>(sp); sp += HeavyNumSmem::kSv;
-  x.bp = reinterpret_cast<uint16_t*>(sp); sp += HeavyNumSmem::kBp;
-  x.wbm = reinterpret_cast<uint32_t*>(sp); sp += HeavyNumSmem::kWbm;
+  uint32_t* dense_tb = reinterpret_cast<uint32_t*>(sp);
+  uint32_t* dense_pref = dense_tb + kWordsDense; sp += HeavyNumSmem::kTb;
+  uint32_t* pwbits = reinterpret_cast<uint32_t*>(sp); sp += HeavyNumSmem::kPw;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(sp); sp += HeavyNumSmem::kHist;
+  uint32_t* kcnt = reinterpret_cast<uint32_t*>(sp); sp += HeavyNumSmem::kKcnt;
   unsigned char* kb = sp; sp += HeavyNumSmem::kK;
-  x.big = reinterpret_cast<uint32_t*>(sp); sp += HeavyNumSmem::kBig;
-  x.scratch = reinterpret_cast<uint32_t*>(sp);
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(sp);
   int64_t* scratch64 = reinterpret_cast<int64_t*>(sp);
   __shared__ int64_t s_row;
-  __shared__ uint32_t s_nbig;
-  x.nbig = &s_nbig;
   uint32_t* wide_bm = reinterpret_cast<uint32_t*>(region);
   uint32_t* wide_pref = wide_bm + kWordsWide;
   double* dense_acc = reinterpret_cast<double*>(region);
-  uint32_t* dense_bm = small;
-  uint32_t* dense_pref = small + kWordsDense;
-  uint32_t* dense_tb = small + 2 * kWordsDense;
 
   for (int i = threadIdx.x; i < kWordsWide; i += kNT) wide_bm[i] = 0;
-  for (int i = threadIdx.x; i < 3 * kWordsDense; i += kNT) small[i] = 0;
-  for (int i = threadIdx.x; i < kCap; i += kNT) x.cntl[i] = 0;
-  for (int i = threadIdx.x; i < (kNT / 32) * kBatchWords; i += kNT) x.wbm[i] = 0;
+  for (int i = threadIdx.x; i < kWordsDense; i += kNT) dense_tb[i] = 0;
+  for (int i = threadIdx.x; i < kCap / 32; i += kNT) pwbits[i] = 0;
+  for (int i = threadIdx.x; i < kCap; i += kNT) kcnt[i] = 0;
   __syncthreads();
   PH_INIT
 
@@ -596,7 +533,7 @@ k_heavy_numeric(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nr
       bool hi_all;
       while (true) {
         hi_all = lo + width > row_hi;
-        S = kstate_segments<kNT>(st, B, nk, (uint32_t)(hi_all ? 0 : lo + width), hi_all, x.scratch);
+        S = kstate_segments<kNT>(st, B, nk, (uint32_t)(hi_all ? 0 : lo + width), hi_all, scratch);
         PH_COUNT(13, 1);
         if (S <= kCap || width == 1) break;
         if (width > kWinDense) {
@@ -623,101 +560,104 @@ k_heavy_numeric(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nr
       const int wcols = (int)(wend - lo);
       const int nwords = (wcols + 31) >> 5;
       if (S <= kCap) {
-        // ---- wide window: one batch, buckets indexed by output rank
-        x.bm = wide_bm;
-        x.wpref = wide_pref;
-        Items it;
-        gather_items(st, B, nk, 0, S, lo, it, x.sv);
+        // ---- wide window: one batch; sort key = column rank
+        uint32_t c[kItems];
+        const int n = stage_items(st, B, nk, 0, S, lo, sv, c);
+#pragma unroll
+        for (int j = 0; j < kItems; ++j)
+          if (j < n) atomicOr(&wide_bm[c[j] >> 5], 1u << (c[j] & 31));
+        __syncthreads();
         PH(1);
-        const uint32_t m = bucket_batch(x, it, nwords);
-        PH(2);
-        if (threadIdx.x == 0) *x.nbig = 0;
+        for (int wd = threadIdx.x; wd < nwords; wd += kNT) wide_pref[wd] = __popc(wide_bm[wd]);
         __syncthreads();
-        for_each_column(x.bm, x.wpref, nwords, m, [&](uint32_t c, uint32_t r) {
-          const uint32_t s0 = r ? x.cntl[r - 1] : 0u, e0 = x.cntl[r];
-          if (e0 - s0 > kSmallBucket) {
-            x.big[atomicAdd(x.nbig, 1u)] = (c << 13) | r;
-          } else {
-            const bool seq = column_seq(ci, lo + c, sem, mb);
-            insertion_sort_u16(x.bp, s0, e0);
-            const double v = bucket_value(x.sv, x.bp, s0, e0, seq, 0.0);
+        const uint32_t m = block_scan_striped<kNT>(wide_pref, nwords, scratch);
+        const uint32_t q0 = threadIdx.x * kItems;
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) {
+          if (j < n) {
+            const uint32_t wd = c[j] >> 5, bit = 1u << (c[j] & 31);
+            const uint32_t r = wide_pref[wd] + __popc(wide_bm[wd] & (bit - 1u));
+            key0[pad_k(q0 + j)] = (uint16_t)r;
+            pay0[pad_k(q0 + j)] = (uint16_t)(q0 + j);
+            atomicAdd(&kcnt[r], 1u);
             const int64_t o = written + r;
-            if (o < out_n) {
-              c_col[out0 + o] = (uint32_t)(lo + c);
-              c_val[out0 + o] = v;
-            }
+            if (o < out_n) c_col[out0 + o] = (uint32_t)(lo + c[j]);   // same value from every contributor
+            if (!column_seq(ci, lo + c[j], sem, mb)) atomicOr(&pwbits[r >> 5], 1u << (r & 31));
           }
-        });
+        }
         __syncthreads();
+        PH(2);
+        radix_pass<true>(key0, pay0, key1, pay1, S, 0, kRadixBits, hist, scratch);
+        radix_pass<false>(key1, pay1, key0, pay0, S, kRadixBits, 13 - kRadixBits, hist, scratch);
+        block_scan_striped<kNT>(kcnt, (int)m, scratch);   // exclusive -> run starts
         PH(3);
-        big_buckets(x, S, [&](uint32_t c, uint32_t r, uint32_t s0, uint32_t e0) {
-          const double v = bucket_value(x.sv, x.bp, s0, e0, column_seq(ci, lo + c, sem, mb), 0.0);
+        for (uint32_t r = threadIdx.x; r < m; r += kNT) {
+          const uint32_t s0 = kcnt[r], e0 = r + 1 < m ? kcnt[r + 1] : S;
+          const bool pw = (pwbits[r >> 5] >> (r & 31)) & 1u;
+          const double v = pw ? run_pairwise(sv, pay0, s0, e0) : run_seq(sv, pay0, s0, e0, 0.0);
           const int64_t o = written + r;
-          if (o < out_n) {
-            c_col[out0 + o] = (uint32_t)(lo + c);
-            c_val[out0 + o] = v;
-          }
-        });
+          if (o < out_n) c_val[out0 + o] = v;
+        }
         __syncthreads();
-        for (int wd = threadIdx.x; wd < nwords; wd += kNT) x.bm[wd] = 0;
-        for (uint32_t r = threadIdx.x; r < m; r += kNT) x.cntl[r] = 0;
+        for (int wd = threadIdx.x; wd < nwords; wd += kNT) wide_bm[wd] = 0;
+        for (uint32_t r = threadIdx.x; r < m; r += kNT) kcnt[r] = 0;
+        for (uint32_t r = threadIdx.x; r < (m + 31) / 32; r += kNT) pwbits[r] = 0;
         written += m;
         PH(15);
       } else {
-        // ---- dense window: batches with a per-column carry (sequential association)
-        x.bm = dense_bm;
-        x.wpref = dense_pref;
+        // ---- dense window: batches sorted by window-local column, per-column carry
         for (uint32_t B0 = 0; B0 < S; B0 += kCap) {
           const uint32_t nb = min((uint32_t)kCap, S - B0);
           PH_COUNT(11, 1);
-          Items it;
-          gather_items(st, B, nk, B0, nb, lo, it, x.sv);
-          PH(4);
-          const uint32_t m = bucket_batch(x, it, nwords);
-          PH(5);
-          if (threadIdx.x == 0) *x.nbig = 0;
-          __syncthreads();
-          for_each_column(x.bm, x.wpref, nwords, m, [&](uint32_t c, uint32_t r) {
-            const uint32_t s0 = r ? x.cntl[r - 1] : 0u, e0 = x.cntl[r];
-            if (e0 - s0 > kSmallBucket) {
-              x.big[atomicAdd(x.nbig, 1u)] = (c << 13) | r;
-            } else {
-              const bool had = (dense_tb[c >> 5] >> (c & 31)) & 1u;
-              insertion_sort_u16(x.bp, s0, e0);
-              dense_acc[c] = bucket_value(x.sv, x.bp, s0, e0, true, had ? dense_acc[c] : 0.0);
+          uint32_t c[kItems];
+          const int n = stage_items(st, B, nk, B0, nb, lo, sv, c);
+          const uint32_t q0 = threadIdx.x * kItems;
+#pragma unroll
+          for (int j = 0; j < kItems; ++j) {
+            if (j < n) {
+              key0[pad_k(q0 + j)] = (uint16_t)c[j];
+              pay0[pad_k(q0 + j)] = (uint16_t)(q0 + j);
+              atomicAdd(&kcnt[c[j]], 1u);
             }
-          });
-          __syncthreads();
-          big_buckets(x, nb, [&](uint32_t c, uint32_t r, uint32_t s0, uint32_t e0) {
-            const bool had = (dense_tb[c >> 5] >> (c & 31)) & 1u;
-            dense_acc[c] = bucket_value(x.sv, x.bp, s0, e0, true, had ? dense_acc[c] : 0.0);
-          });
-          __syncthreads();
-          for (int wd = threadIdx.x; wd < nwords; wd += kNT) {
-            dense_tb[wd] |= x.bm[wd];
-            x.bm[wd] = 0;
           }
-          for (uint32_t r = threadIdx.x; r < m; r += kNT) x.cntl[r] = 0;
           __syncthreads();
+          PH(4);
+          radix_pass<true>(key0, pay0, key1, pay1, nb, 0, 6, hist, scratch);
+          radix_pass<false>(key1, pay1, key0, pay0, nb, 6, 6, hist, scratch);
+          block_scan_striped<kNT>(kcnt, wcols, scratch);
+          PH(5);
+          for (int cc = threadIdx.x; cc < wcols; cc += kNT) {
+            const uint32_t s0 = kcnt[cc], e0 = cc + 1 < wcols ? kcnt[cc + 1] : nb;
+            if (e0 == s0) continue;
+            const uint32_t bit = 1u << (cc & 31);
+            const bool had = (dense_tb[cc >> 5] & bit) != 0u;
+            dense_acc[cc] = run_seq(sv, pay0, s0, e0, had ? dense_acc[cc] : 0.0);
+            if (!had) atomicOr(&dense_tb[cc >> 5], bit);
+          }
+          __syncthreads();
+          for (int cc = threadIdx.x; cc < wcols; cc += kNT) kcnt[cc] = 0;
           PH(6);
         }
         // emit every column touched by the window, ascending
-        for (int wd = threadIdx.x; wd < nwords; wd += kNT) x.wpref[wd] = __popc(dense_tb[wd]);
+        for (int wd = threadIdx.x; wd < nwords; wd += kNT) dense_pref[wd] = __popc(dense_tb[wd]);
         __syncthreads();
-        const uint32_t nout = block_scan_striped<kNT>(x.wpref, nwords, x.scratch);
-        for (int c = threadIdx.x; c < wcols; c += kNT) {
-          const uint32_t word = dense_tb[c >> 5], bit = 1u << (c & 31);
+        const uint32_t nout = block_scan_striped<kNT>(dense_pref, nwords, scratch);
+        for (int cc = threadIdx.x; cc < wcols; cc += kNT) {
+          const uint32_t word = dense_tb[cc >> 5], bit = 1u << (cc & 31);
           if (word & bit) {
-            const int64_t o = written + x.wpref[c >> 5] + __popc(word & (bit - 1u));
+            const int64_t o = written + dense_pref[cc >> 5] + __popc(word & (bit - 1u));
             if (o < out_n) {
-              c_col[out0 + o] = (uint32_t)(lo + c);
-              c_val[out0 + o] = dense_acc[c];
+              c_col[out0 + o] = (uint32_t)(lo + cc);
+              c_val[out0 + o] = dense_acc[cc];
             }
           }
         }
         __syncthreads();
+        // the carry overwrote the wide bitmap: clear the slots it used, then the touched bits
+        for (int cc = threadIdx.x; cc < wcols; cc += kNT)
+          if ((dense_tb[cc >> 5] >> (cc & 31)) & 1u) dense_acc[cc] = 0.0;
+        __syncthreads();
         for (int wd = threadIdx.x; wd < nwords; wd += kNT) dense_tb[wd] = 0;
-        for (int q = threadIdx.x; q < kWordsWide * 2; q += kNT) wide_bm[q] = 0;   // region back to a clean bitmap
         written += nout;
         PH(7);
       }

@@ -62,6 +62,7 @@ mg::DevCsr dev_csr(const magnus_csr& m) {
   d.rp32 = m.rp_bytes == 4 ? static_cast<const int32_t*>(m.row_ptr) : nullptr;
   d.col = m.col;
   d.val = m.val;
+  d.skip = nullptr;
   return d;
 }
 
@@ -95,6 +96,7 @@ struct magnus_ctx {
   unsigned long long* err = nullptr;
   int64_t* counts = nullptr;
   int64_t* tile_sums = nullptr;
+  uint32_t* skip = nullptr;
   uint32_t* modebits = nullptr;
   uint32_t* gk = nullptr;
   uint32_t* gchunk = nullptr;
@@ -293,6 +295,18 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   MG_CUDA(ctx->alloc(&ctx->err, 2));
   MG_CUDA(cudaMemsetAsync(ctx->stats, 0, mg::kStatLen * 8, s));
   MG_CUDA(cudaMemsetAsync(ctx->err, 0, 16, s));
+  {
+    const int64_t nskip = (B->nnz + 31) / 32;
+    MG_CUDA(ctx->alloc(&ctx->skip, nskip + 1));
+    if (nskip > 0) {
+      mg::k_build_skip<<<(unsigned)std::min<int64_t>((nskip + 255) / 256, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+          B->col, B->nnz, ctx->skip);
+      MG_CUDA(cudaGetLastError());
+      ++ctx->launches;
+    }
+    ctx->B.skip = ctx->skip;
+    if (A->row_ptr == B->row_ptr && A->col == B->col) ctx->A.skip = ctx->skip;
+  }
   if (n > 0) {
     ctx->begin(MAGNUS_K_ROW_STATS);
     rc = magnus_row_stats(A, B, ctx->inter, ctx->mn, ctx->mx, stream);
@@ -378,7 +392,7 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
   const int64_t nW = ctx->host_stats[mg::kStatNW], nB = ctx->host_stats[mg::kStatNB], nH = ctx->host_stats[mg::kStatNH];
   if (nH > 0) {
     MG_CUDA(cudaMemsetAsync(ctx->work, 0, 8, s));
-    const unsigned grid = (unsigned)std::min<int64_t>(nH, numeric ? 2 * ctx->sm_count : ctx->sm_count);
+    const unsigned grid = (unsigned)std::min<int64_t>(nH, ctx->sm_count);
     ctx->begin(numeric ? MAGNUS_K_NUM_HEAVY : MAGNUS_K_SYM_HEAVY);
     if (numeric)
       mg::k_heavy_numeric<<<grid, mg::kNT, mg::HeavyNumSmem::kTotal, s>>>(

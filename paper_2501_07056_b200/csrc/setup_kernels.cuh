@@ -89,6 +89,13 @@ __global__ void k_categorize(int64_t n, DevCsr A, const int64_t* __restrict__ in
   }
 }
 
+// skip list of B: skip[j] = col[32*j]
+__global__ void k_build_skip(const uint32_t* __restrict__ col, int64_t nnz, uint32_t* __restrict__ skip) {
+  const int64_t n = (nnz + 31) / 32;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    skip[j] = __ldg(col + 32 * j);
+}
+
 // ---------------------------------------------------------------- device-wide exclusive scan (int64)
 constexpr int kScanT = 512, kScanItems = 16, kScanTile = kScanT * kScanItems;
 

@@ -30,9 +30,9 @@ L.magnus_debug_phases(out, 1)
 Cm, _ = plan.numeric(rp)
 print(plan.ctx.profile_read())
 L.magnus_debug_phases(out, 1)
-names = ["choose window", "wide gather", "wide bucket", "wide small", "dense gather", "dense bucket", "dense reduce",
-         "dense emit", "advance", "row load", "#windows", "#dense batches", "#rows nk>1024", "#segment passes",
-         "#elements", "wide big"]
+names = ["choose window", "wide stage+mark", "wide rank", "wide sort", "dense stage", "dense sort", "dense reduce",
+         "dense emit", "advance", "row load", "#windows", "#dense batches", "#rows nk>512", "#segment passes",
+         "#elements", "wide reduce"]
 timers = [0, 1, 2, 3, 15, 4, 5, 6, 7, 8, 9]
 tot = sum(out[i] for i in timers)
 for i in timers + [10, 11, 12, 13, 14]:
