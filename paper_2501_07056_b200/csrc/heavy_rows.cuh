@@ -37,12 +37,12 @@ __device__ unsigned long long g_phase[32];
 #endif
 
 constexpr int kHT = 512;                // symbolic: threads per CTA (1 CTA / SM)
-constexpr int kNT = 512;                // numeric: threads per CTA (1 CTA / SM)
+constexpr int kNT = 1024;               // numeric: threads per CTA (1 CTA / SM, 32 warps)
 constexpr int kCap = 8192;              // numeric: stream elements per batch
 constexpr int kItems = kCap / kNT;      // 16 stream elements per thread per batch
 constexpr int kSymItems = 16;           // symbolic: stream elements per thread per tile
 constexpr int kKS = 1024;               // symbolic: k's whose cursors live in shared memory
-constexpr int kKSN = 512;               // numeric: k's whose cursors live in shared memory
+constexpr int kKSN = 256;               // numeric: k's whose cursors live in shared memory
 constexpr int kSymWin = 1 << 20;        // symbolic window width (columns; 128 KB bitmap)
 constexpr int kChunkSmem = 8192;        // numeric-plan chunk counters kept in smem (symbolic)
 
@@ -114,15 +114,18 @@ struct KState {
   uint32_t* koff;  // nk + 1
   uint32_t* kend;
   double* kav;
+  uint32_t* knext;  // column at the cursor (0xffffffff when the B row is exhausted)
 };
 
 template <int T>
 __device__ __forceinline__ void kstate_load(const KState& st, const DevCsr& A, const DevCsr& B, int64_t a0, int nk) {
   for (int t = threadIdx.x; t < nk; t += T) {
     const int64_t k = __ldg(A.col + a0 + t);
-    st.ks[t] = (uint32_t)B.rp(k);
-    st.kend[t] = (uint32_t)B.rp(k + 1);
+    const uint32_t b0 = (uint32_t)B.rp(k), b1 = (uint32_t)B.rp(k + 1);
+    st.ks[t] = b0;
+    st.kend[t] = b1;
     st.kav[t] = __ldg(A.val + a0 + t);
+    st.knext[t] = b0 < b1 ? __ldg(B.col + b0) : 0xffffffffu;
   }
 }
 
@@ -133,7 +136,8 @@ __device__ __forceinline__ uint32_t kstate_segments(const KState& st, const DevC
                                                     uint32_t* scratch) {
   for (int t = threadIdx.x; t < nk; t += T) {
     const uint32_t s = st.ks[t], e0 = st.kend[t];
-    const uint32_t e = hi_all ? e0 : gallop_col(B, s, e0, hi);
+    // a k whose next column is already past the window contributes nothing: no search
+    const uint32_t e = hi_all ? e0 : (st.knext[t] >= hi ? s : gallop_col(B, s, e0, hi));
     st.ke[t] = e;
     st.koff[t] = e - s;
   }
@@ -150,11 +154,12 @@ __device__ __forceinline__ int64_t kstate_advance(const KState& st, const DevCsr
   int64_t nxt = INT64_MAX;
   for (int t = threadIdx.x; t < nk; t += T) {
     const uint32_t e = st.ke[t];
-    st.ks[t] = e;
-    if (e < st.kend[t]) {
-      const int64_t c = __ldg(B.col + e);
-      nxt = c < nxt ? c : nxt;
+    if (e != st.ks[t]) {
+      st.ks[t] = e;
+      st.knext[t] = e < st.kend[t] ? __ldg(B.col + e) : 0xffffffffu;
     }
+    const uint32_t c = st.knext[t];
+    if (c != 0xffffffffu && (int64_t)c < nxt) nxt = c;
   }
   return block_min_i64<T>(nxt, scratch64);
 }
@@ -177,7 +182,7 @@ __device__ __forceinline__ int kstate_find(const KState& st, int nk, uint32_t p)
 struct HeavySymSmem {
   static constexpr size_t kBitmap = (kSymWin / 32) * 4;                 // 128 KB
   static constexpr size_t kChunk = kChunkSmem * 4;                       // 32 KB
-  static constexpr size_t kK = (size_t)kKS * 4 * 4 + (kKS + 4) * 4 + kKS * 8;
+  static constexpr size_t kK = (size_t)kKS * 4 * 5 + (kKS + 4) * 4 + kKS * 8;
   static constexpr size_t kScratch = 64 * 8;
   static constexpr size_t kTotal = kBitmap + kChunk + kK + kScratch;
   static_assert(kBitmap % 16 == 0 && kChunk % 16 == 0 && kK % 16 == 0, "16-byte aligned sections");
@@ -219,13 +224,15 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
       st.kend = st.ke + kKS;
       st.koff = st.kend + kKS;
       st.kav = reinterpret_cast<double*>(st.koff + kKS + 4);
+      st.knext = reinterpret_cast<uint32_t*>(st.kav + kKS);
     } else {
-      uint32_t* g = gk + (size_t)blockIdx.x * (size_t)gk_stride * 6;
+      uint32_t* g = gk + (size_t)blockIdx.x * (size_t)gk_stride * 7;
       st.ks = g;
       st.ke = g + gk_stride;
       st.kend = g + 2 * gk_stride;
       st.koff = g + 3 * gk_stride;
       st.kav = reinterpret_cast<double*>(g + 4 * gk_stride);
+      st.knext = g + 6 * gk_stride;
     }
     kstate_load<kHT>(st, A, B, a0, nk);
     const int ci = cat[i];
@@ -309,10 +316,10 @@ constexpr int kRadix = 1 << kRadixBits;     // 128 digits
 constexpr int kNW = kNT / 32;               // 16 warps
 constexpr int kWaves = kCap / kNT;          // 16 waves of 32 per warp
 
-// Staging layouts are written blocked (thread t owns positions 16t..16t+15) and read
-// lane-consecutive; one pad slot per 16 entries keeps both bank-conflict free.
-__device__ __forceinline__ uint32_t pad_v(uint32_t q) { return q + (q >> 4); }          // doubles
-__device__ __forceinline__ uint32_t pad_k(uint32_t q) { return q + ((q >> 4) << 1); }   // u16 pairs
+// Staging is lane-consecutive (item v of thread t = position v*kNT + t): coalesced
+// reads of B and conflict-free shared-memory stores, no padding needed.
+__device__ __forceinline__ uint32_t pad_v(uint32_t q) { return q; }
+__device__ __forceinline__ uint32_t pad_k(uint32_t q) { return q; }
 
 // true: the reference's dense accumulator (sequential from +0.0); false: its sort accumulator
 __device__ __forceinline__ bool column_seq(int ci, int64_t col, const Sem& sem, const uint32_t* __restrict__ mb) {
@@ -408,7 +415,7 @@ struct HeavyNumSmem {
   static constexpr size_t kPw = (size_t)(kCap / 32) * 4;            // wide: pairwise flag per rank
   static constexpr size_t kHist = (size_t)kRadix * kNW * 4;         // 8 KB
   static constexpr size_t kKcnt = (size_t)kCap * 4;                 // 32 KB elements per sort key -> run starts
-  static constexpr size_t kK = (size_t)kKSN * 4 * 4 + (kKSN + 4) * 4 + kKSN * 8;
+  static constexpr size_t kK = (size_t)kKSN * 4 * 5 + (kKSN + 4) * 4 + kKSN * 8;
   static constexpr size_t kScratch = 64 * 8;
   static constexpr size_t kTotal = kSv + kKeys + kPays + kRegion + kTb + kPw + kHist + kKcnt + kK + kScratch;
   static_assert(kSv % 16 == 0 && kKeys % 16 == 0 && kPays % 16 == 0 && kRegion % 16 == 0 && kTb % 16 == 0 &&
@@ -418,32 +425,31 @@ struct HeavyNumSmem {
 };
 
 // Stage stream positions [B0, B0 + nb) of the window: value into sv[q]; window-local
-// column returned in c[] (q = position in the batch = threadIdx.x * kItems + j).
-__device__ __forceinline__ int stage_items(const KState& st, const DevCsr& B, int nk, uint32_t B0, uint32_t nb, int64_t lo,
-                                           double* sv, uint32_t* c) {
-  const uint32_t q0 = threadIdx.x * kItems;
-  const int n = q0 < nb ? (int)min((uint32_t)kItems, nb - q0) : 0;
+// column returned in c[v] for q = v*kNT + threadIdx.x (lane-consecutive: a warp reads
+// 32 consecutive stream positions, i.e. contiguous pieces of B rows -> coalesced).
+__device__ __forceinline__ void stage_items(const KState& st, const DevCsr& B, int nk, uint32_t B0, uint32_t nb, int64_t lo,
+                                            double* sv, uint32_t* c) {
   uint32_t pos[kItems];
   int tk[kItems];
-  if (n > 0) {
-    int t = kstate_find(st, nk, B0 + q0);
 #pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-      if (j < n) {
-        const uint32_t p = B0 + q0 + j;
-        while (st.koff[t + 1] <= p) ++t;
-        pos[j] = st.ks[t] + (p - st.koff[t]);
-        tk[j] = t;
-      }
+  for (int v = 0; v < kItems; ++v) {
+    const uint32_t q = v * kNT + threadIdx.x;
+    if (q < nb) {
+      const int t = kstate_find(st, nk, B0 + q);
+      pos[v] = st.ks[t] + (B0 + q - st.koff[t]);
+      tk[v] = t;
     }
   }
 #pragma unroll
-  for (int j = 0; j < kItems; ++j)
-    if (j < n) c[j] = (uint32_t)((int64_t)__ldg(B.col + pos[j]) - lo);
+  for (int v = 0; v < kItems; ++v) {
+    const uint32_t q = v * kNT + threadIdx.x;
+    if (q < nb) c[v] = (uint32_t)((int64_t)__ldg(B.col + pos[v]) - lo);
+  }
 #pragma unroll
-  for (int j = 0; j < kItems; ++j)
-    if (j < n) sv[pad_v(q0 + j)] = __dmul_rn(st.kav[tk[j]], __ldg(B.val + pos[j]));
-  return n;
+  for (int v = 0; v < kItems; ++v) {
+    const uint32_t q = v * kNT + threadIdx.x;
+    if (q < nb) sv[q] = __dmul_rn(st.kav[tk[v]], __ldg(B.val + pos[v]));
+  }
 }
 
 // After the sort, key k's run is [kcnt[k-1], kcnt[k]) (kcnt = inclusive prefix of the
@@ -507,13 +513,15 @@ k_heavy_numeric(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nr
       st.kend = st.ke + kKSN;
       st.koff = st.kend + kKSN;
       st.kav = reinterpret_cast<double*>(st.koff + kKSN + 4);
+      st.knext = reinterpret_cast<uint32_t*>(st.kav + kKSN);
     } else {
-      uint32_t* g = gk + (size_t)blockIdx.x * (size_t)gk_stride * 6;
+      uint32_t* g = gk + (size_t)blockIdx.x * (size_t)gk_stride * 7;
       st.ks = g;
       st.ke = g + gk_stride;
       st.kend = g + 2 * gk_stride;
       st.koff = g + 3 * gk_stride;
       st.kav = reinterpret_cast<double*>(g + 4 * gk_stride);
+      st.knext = g + 6 * gk_stride;
       PH_COUNT(12, 1);
     }
     PH(9);
@@ -562,44 +570,69 @@ k_heavy_numeric(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nr
       if (S <= kCap) {
         // ---- wide window: one batch; sort key = column rank
         uint32_t c[kItems];
-        const int n = stage_items(st, B, nk, 0, S, lo, sv, c);
+        stage_items(st, B, nk, 0, S, lo, sv, c);
 #pragma unroll
-        for (int j = 0; j < kItems; ++j)
-          if (j < n) atomicOr(&wide_bm[c[j] >> 5], 1u << (c[j] & 31));
+        for (int v = 0; v < kItems; ++v)
+          if (v * kNT + threadIdx.x < S) atomicOr(&wide_bm[c[v] >> 5], 1u << (c[v] & 31));
         __syncthreads();
         PH(1);
         for (int wd = threadIdx.x; wd < nwords; wd += kNT) wide_pref[wd] = __popc(wide_bm[wd]);
         __syncthreads();
         const uint32_t m = block_scan_striped<kNT>(wide_pref, nwords, scratch);
-        const uint32_t q0 = threadIdx.x * kItems;
 #pragma unroll
-        for (int j = 0; j < kItems; ++j) {
-          if (j < n) {
-            const uint32_t wd = c[j] >> 5, bit = 1u << (c[j] & 31);
+        for (int v = 0; v < kItems; ++v) {
+          if (v * kNT + threadIdx.x < S) {
+            const uint32_t wd = c[v] >> 5, bit = 1u << (c[v] & 31);
             const uint32_t r = wide_pref[wd] + __popc(wide_bm[wd] & (bit - 1u));
-            key0[pad_k(q0 + j)] = (uint16_t)r;
-            pay0[pad_k(q0 + j)] = (uint16_t)(q0 + j);
             atomicAdd(&kcnt[r], 1u);
             const int64_t o = written + r;
-            if (o < out_n) c_col[out0 + o] = (uint32_t)(lo + c[j]);   // same value from every contributor
-            if (!column_seq(ci, lo + c[j], sem, mb)) atomicOr(&pwbits[r >> 5], 1u << (r & 31));
+            if (o < out_n) c_col[out0 + o] = (uint32_t)(lo + c[v]);   // same value from every contributor
+            if (!column_seq(ci, lo + c[v], sem, mb)) atomicOr(&pwbits[r >> 5], 1u << (r & 31));
+            c[v] = r;   // keep the rank for the election
           }
         }
         __syncthreads();
         PH(2);
-        radix_pass<true>(key0, pay0, key1, pay1, S, 0, kRadixBits, hist, scratch);
-        radix_pass<false>(key1, pay1, key0, pay0, S, kRadixBits, 13 - kRadixBits, hist, scratch);
-        block_scan_striped<kNT>(kcnt, (int)m, scratch);   // exclusive -> run starts
+        // Stable bucketing by rank without a sort: positions are visited in stream
+        // (ascending-k) order in waves of kNT; inside a wave, positions sharing a
+        // rank take their bucket slots one election round at a time (lowest
+        // position first).  Wide windows rarely repeat a column inside a wave.
+        block_scan_striped<kNT>(kcnt, (int)m, scratch);   // exclusive: bucket starts = fill cursors
+        uint32_t* tag = wide_bm;                           // per-rank election tag (bitmap no longer needed)
+        uint16_t* bucket = pay1;                           // positions, bucket-ordered
+        for (uint32_t r = threadIdx.x; r < m; r += kNT) tag[r] = 0xffffffffu;
+        __syncthreads();
+#pragma unroll
+        for (int v = 0; v < kItems; ++v) {
+          const uint32_t p0 = v * kNT;
+          if (p0 >= S) break;
+          const uint32_t p = p0 + threadIdx.x;
+          bool pending = p < S;
+          const uint32_t r = pending ? c[v] : 0u;
+          while (true) {
+            if (pending) atomicMin(&tag[r], p);
+            __syncthreads();
+            const bool win = pending && tag[r] == p;
+            if (win) bucket[kcnt[r]++] = (uint16_t)p;
+            __syncthreads();
+            if (win) {
+              tag[r] = 0xffffffffu;
+              pending = false;
+            }
+            if (!__syncthreads_or(pending)) break;
+          }
+        }
+        // kcnt[r] is now the end of bucket r
         PH(3);
         for (uint32_t r = threadIdx.x; r < m; r += kNT) {
-          const uint32_t s0 = kcnt[r], e0 = r + 1 < m ? kcnt[r + 1] : S;
+          const uint32_t s0 = r ? kcnt[r - 1] : 0u, e0 = kcnt[r];
           const bool pw = (pwbits[r >> 5] >> (r & 31)) & 1u;
-          const double v = pw ? run_pairwise(sv, pay0, s0, e0) : run_seq(sv, pay0, s0, e0, 0.0);
+          const double v = pw ? run_pairwise(sv, bucket, s0, e0) : run_seq(sv, bucket, s0, e0, 0.0);
           const int64_t o = written + r;
           if (o < out_n) c_val[out0 + o] = v;
         }
         __syncthreads();
-        for (int wd = threadIdx.x; wd < nwords; wd += kNT) wide_bm[wd] = 0;
+        for (uint32_t wd = threadIdx.x; wd < max((uint32_t)nwords, m); wd += kNT) wide_bm[wd] = 0;
         for (uint32_t r = threadIdx.x; r < m; r += kNT) kcnt[r] = 0;
         for (uint32_t r = threadIdx.x; r < (m + 31) / 32; r += kNT) pwbits[r] = 0;
         written += m;
@@ -610,19 +643,19 @@ k_heavy_numeric(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nr
           const uint32_t nb = min((uint32_t)kCap, S - B0);
           PH_COUNT(11, 1);
           uint32_t c[kItems];
-          const int n = stage_items(st, B, nk, B0, nb, lo, sv, c);
-          const uint32_t q0 = threadIdx.x * kItems;
+          stage_items(st, B, nk, B0, nb, lo, sv, c);
 #pragma unroll
-          for (int j = 0; j < kItems; ++j) {
-            if (j < n) {
-              key0[pad_k(q0 + j)] = (uint16_t)c[j];
-              pay0[pad_k(q0 + j)] = (uint16_t)(q0 + j);
-              atomicAdd(&kcnt[c[j]], 1u);
+          for (int v = 0; v < kItems; ++v) {
+            const uint32_t q = v * kNT + threadIdx.x;
+            if (q < nb) {
+              key0[q] = (uint16_t)c[v];
+              pay0[q] = (uint16_t)q;
+              atomicAdd(&kcnt[c[v]], 1u);
             }
           }
           __syncthreads();
           PH(4);
-          radix_pass<true>(key0, pay0, key1, pay1, nb, 0, 6, hist, scratch);
+          radix_pass<false>(key0, pay0, key1, pay1, nb, 0, 6, hist, scratch);
           radix_pass<false>(key1, pay1, key0, pay0, nb, 6, 6, hist, scratch);
           block_scan_striped<kNT>(kcnt, wcols, scratch);
           PH(5);

@@ -371,7 +371,7 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   MG_CUDA(ctx->alloc(&ctx->modebits, std::max<int64_t>(1, nH) * ctx->sem.mode_words));
   const int64_t maxnk = ctx->host_stats[mg::kStatMaxNk];
   ctx->gk_stride = maxnk > mg::kKSN ? ((maxnk + 8) / 4) * 4 : 4;
-  MG_CUDA(ctx->alloc(&ctx->gk, (size_t)2 * ctx->sm_count * ctx->gk_stride * 6));
+  MG_CUDA(ctx->alloc(&ctx->gk, (size_t)2 * ctx->sm_count * ctx->gk_stride * 7));
   const bool chunk_global = n_chunks_global > mg::kChunkSmem;
   MG_CUDA(ctx->alloc(&ctx->gchunk, chunk_global ? (size_t)ctx->sm_count * n_chunks_global : 1));
   if (chunk_global) MG_CUDA(cudaMemsetAsync(ctx->gchunk, 0, (size_t)ctx->sm_count * n_chunks_global * 4, s));

@@ -30,7 +30,7 @@ L.magnus_debug_phases(out, 1)
 Cm, _ = plan.numeric(rp)
 print(plan.ctx.profile_read())
 L.magnus_debug_phases(out, 1)
-names = ["choose window", "wide stage+mark", "wide rank", "wide sort", "dense stage", "dense sort", "dense reduce",
+names = ["choose window", "wide stage+mark", "wide rank", "wide elect", "dense stage", "dense sort", "dense reduce",
          "dense emit", "advance", "row load", "#windows", "#dense batches", "#rows nk>512", "#segment passes",
          "#elements", "wide reduce"]
 timers = [0, 1, 2, 3, 15, 4, 5, 6, 7, 8, 9]
