@@ -37,8 +37,8 @@ __device__ unsigned long long g_phase[32];
 #endif
 
 constexpr int kHT = 512;                // symbolic: threads per CTA (1 CTA / SM)
-constexpr int kNT = 1024;               // numeric: threads per CTA (1 CTA / SM, 32 warps)
-constexpr int kCap = 8192;              // numeric: stream elements per batch
+constexpr int kNT = 512;                // numeric: threads per CTA (2 CTAs / SM, 32 warps)
+constexpr int kCap = 4096;              // numeric: stream elements per batch
 constexpr int kItems = kCap / kNT;      // 16 stream elements per thread per batch
 constexpr int kSymItems = 16;           // symbolic: stream elements per thread per tile
 constexpr int kKS = 1024;               // symbolic: k's whose cursors live in shared memory
@@ -307,12 +307,12 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
 //    only -- windows holding pairwise columns are narrowed until they fit one
 //    batch): key = window-local column (12 bits), runs add into a per-column
 //    carry; the touched columns are emitted when the window is done.
-constexpr int kWinWide = 1 << 17;
-constexpr int kWinDense = 4096;
-constexpr int kWordsWide = kWinWide / 32;   // 4096
-constexpr int kWordsDense = kWinDense / 32; // 128
-constexpr int kRadixBits = 7;
-constexpr int kRadix = 1 << kRadixBits;     // 128 digits
+constexpr int kWinWide = 1 << 16;
+constexpr int kWinDense = 2048;
+constexpr int kWordsWide = kWinWide / 32;   // 2048
+constexpr int kWordsDense = kWinDense / 32; // 64
+constexpr int kRadixBits = 6;
+constexpr int kRadix = 1 << kRadixBits;     // 64 digits
 constexpr int kNW = kNT / 32;               // 16 warps
 constexpr int kWaves = kCap / kNT;          // 16 waves of 32 per warp
 
@@ -407,9 +407,9 @@ __device__ __forceinline__ void radix_pass(const uint16_t* kin, const uint16_t* 
 }
 
 struct HeavyNumSmem {
-  static constexpr size_t kSv = (size_t)(kCap + kCap / 16) * 8;    // 68 KB values by (padded) stream position
-  static constexpr size_t kKeys = (size_t)(kCap + kCap / 8 + kCap) * 2;   // 34 KB sort keys: padded in | out
-  static constexpr size_t kPays = (size_t)(kCap + kCap / 8 + kCap) * 2;   // 34 KB payloads = stream positions
+  static constexpr size_t kSv = (size_t)kCap * 8;                  // values by stream position
+  static constexpr size_t kKeys = (size_t)kCap * 2 * 2;             // sort keys (ping-pong)
+  static constexpr size_t kPays = (size_t)kCap * 2 * 2;             // payloads = stream positions
   static constexpr size_t kRegion = (size_t)kWordsWide * 4 * 2;     // 32 KB wide bitmap+prefix | dense carry
   static constexpr size_t kTb = (size_t)kWordsDense * 4 * 2;        // dense touched bitmap + prefix
   static constexpr size_t kPw = (size_t)(kCap / 32) * 4;            // wide: pairwise flag per rank
@@ -421,7 +421,7 @@ struct HeavyNumSmem {
   static_assert(kSv % 16 == 0 && kKeys % 16 == 0 && kPays % 16 == 0 && kRegion % 16 == 0 && kTb % 16 == 0 &&
                     kPw % 16 == 0 && kHist % 16 == 0 && kK % 16 == 0,
                 "shared-memory sections must keep 16-byte alignment");
-  static_assert(kTotal <= 232448, "fits the 227 KB opt-in shared memory of a B200 CTA");
+  static_assert(kTotal <= 113 * 1024, "two CTAs per SM (228 KB shared memory per SM)");
 };
 
 // Stage stream positions [B0, B0 + nb) of the window: value into sv[q]; window-local
@@ -463,7 +463,7 @@ __device__ __forceinline__ void for_each_key(const uint32_t* kcnt, uint32_t nkey
   }
 }
 
-__global__ void __launch_bounds__(kNT, 1)
+__global__ void __launch_bounds__(kNT, 2)
 k_heavy_numeric(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows, const int8_t* __restrict__ cat,
                 const int64_t* __restrict__ mn, const int64_t* __restrict__ mx, Sem sem,
                 const uint32_t* __restrict__ modebits, const int64_t* __restrict__ c_rp, uint32_t* __restrict__ c_col,
@@ -473,9 +473,9 @@ k_heavy_numeric(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nr
   unsigned char* sp = smem;
   double* sv = reinterpret_cast<double*>(sp); sp += HeavyNumSmem::kSv;
   uint16_t* key0 = reinterpret_cast<uint16_t*>(sp);
-  uint16_t* key1 = key0 + kCap + kCap / 8; sp += HeavyNumSmem::kKeys;
+  uint16_t* key1 = key0 + kCap; sp += HeavyNumSmem::kKeys;
   uint16_t* pay0 = reinterpret_cast<uint16_t*>(sp);
-  uint16_t* pay1 = pay0 + kCap + kCap / 8; sp += HeavyNumSmem::kPays;
+  uint16_t* pay1 = pay0 + kCap; sp += HeavyNumSmem::kPays;
   unsigned char* region = sp; sp += HeavyNumSmem::kRegion;
   uint32_t* dense_tb = reinterpret_cast<uint32_t*>(sp);
   uint32_t* dense_pref = dense_tb + kWordsDense; sp += HeavyNumSmem::kTb;
@@ -656,7 +656,7 @@ k_heavy_numeric(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nr
           __syncthreads();
           PH(4);
           radix_pass<false>(key0, pay0, key1, pay1, nb, 0, 6, hist, scratch);
-          radix_pass<false>(key1, pay1, key0, pay0, nb, 6, 6, hist, scratch);
+          radix_pass<false>(key1, pay1, key0, pay0, nb, 6, 5, hist, scratch);
           block_scan_striped<kNT>(kcnt, wcols, scratch);
           PH(5);
           for (int cc = threadIdx.x; cc < wcols; cc += kNT) {

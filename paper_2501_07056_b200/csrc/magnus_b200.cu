@@ -392,7 +392,7 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
   const int64_t nW = ctx->host_stats[mg::kStatNW], nB = ctx->host_stats[mg::kStatNB], nH = ctx->host_stats[mg::kStatNH];
   if (nH > 0) {
     MG_CUDA(cudaMemsetAsync(ctx->work, 0, 8, s));
-    const unsigned grid = (unsigned)std::min<int64_t>(nH, ctx->sm_count);
+    const unsigned grid = (unsigned)std::min<int64_t>(nH, numeric ? 2 * ctx->sm_count : ctx->sm_count);
     ctx->begin(numeric ? MAGNUS_K_NUM_HEAVY : MAGNUS_K_SYM_HEAVY);
     if (numeric)
       mg::k_heavy_numeric<<<grid, mg::kNT, mg::HeavyNumSmem::kTotal, s>>>(
