@@ -127,7 +127,8 @@ def algorithmic_bytes(A, B, inter, c_nnz_row, rp_bytes_a, rp_bytes_b):
     compulsory model restricted to the rows a kernel processes."""
     import torch
     nk = (A.row_ptr[1:] - A.row_ptr[:-1]).to(torch.int64)
-    classes = {"warp": (inter > 0) & (inter <= 256), "block": (inter > 256) & (inter <= 4096), "heavy": inter > 4096}
+    classes = {"warp": (inter > 0) & (inter <= 256), "block": (inter > 256) & (inter <= 4096), "heavy": inter > 4096,
+               "dense": inter > 0}
     out = {}
     for name, m in classes.items():
         nkm = int(nk[m].sum())
@@ -229,7 +230,7 @@ def main():
     sysp = detect_device_params()
     stats = row_intermediate_stats(A, B)
     inter = stats.inter_size
-    cuts, total_inter = flop_split(inter, world)
+    cuts, total_inter = flop_cuts(inter, world)
     lo, hi = cuts[rank], cuts[rank + 1]
     A_loc = row_block(A, lo, hi) if world > 1 else A
 
@@ -287,6 +288,7 @@ def main():
     del C
     peak, peak_kind = hbm_peak()
     kern_bytes = {"num_heavy": ab["heavy"]["num_bytes"], "sym_heavy": ab["heavy"]["sym_bytes"],
+                  "num_dense": ab["dense"]["num_bytes"], "sym_dense": ab["dense"]["sym_bytes"],
                   "num_block": ab["block"]["num_bytes"], "sym_block": ab["block"]["sym_bytes"],
                   "num_warp": ab["warp"]["num_bytes"], "sym_warp": ab["warp"]["sym_bytes"]}
     dom = max(prof, key=lambda k: prof[k][0])

@@ -14,6 +14,7 @@
 
 #include "../../include/magnus_b200.h"
 #include "common.cuh"
+#include "dense_rows.cuh"
 #include "heavy_rows.cuh"
 #include "setup_kernels.cuh"
 #include "small_rows.cuh"
@@ -91,6 +92,7 @@ struct magnus_ctx {
   int32_t* listB = nullptr;
   int32_t* listH = nullptr;
   int32_t* listCoarse = nullptr;
+  int32_t* listD = nullptr;
   unsigned long long* stats = nullptr;   // kStatLen
   unsigned long long* work = nullptr;    // work counters (4)
   unsigned long long* err = nullptr;
@@ -219,6 +221,10 @@ int magnus_ctx_create(magnus_ctx** out) {
   MG_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
   MG_CUDA(cudaFuncSetAttribute(mg::k_rows_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mg::kBSmem));
   MG_CUDA(cudaFuncSetAttribute(mg::k_rows_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mg::kBSmem));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_rows_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)mg::DenseRowSmem::kTotal));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_rows_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)mg::DenseRowSmem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_heavy_symbolic, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::HeavySymSmem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_heavy_numeric, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -290,6 +296,7 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   MG_CUDA(ctx->alloc(&ctx->listB, n + 1));
   MG_CUDA(ctx->alloc(&ctx->listH, n + 1));
   MG_CUDA(ctx->alloc(&ctx->listCoarse, n + 1));
+  MG_CUDA(ctx->alloc(&ctx->listD, n + 1));
   MG_CUDA(ctx->alloc(&ctx->stats, mg::kStatLen));
   MG_CUDA(ctx->alloc(&ctx->work, 8));
   MG_CUDA(ctx->alloc(&ctx->err, 2));
@@ -316,7 +323,7 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sm_count * 16);
     ctx->begin(MAGNUS_K_CATEGORIZE);
     mg::k_categorize<<<grid, 256, 0, s>>>(n, ctx->A, ctx->inter, ctx->mn, ctx->mx, cp, ctx->cat, ctx->listW, ctx->listB,
-                                          ctx->listH, ctx->listCoarse, ctx->stats);
+                                          ctx->listH, ctx->listCoarse, ctx->listD, ctx->stats);
     ctx->end();
     MG_CUDA(cudaGetLastError());
   }
@@ -414,6 +421,22 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
     else
       mg::k_rows_block<false><<<grid, mg::kBT, mg::kBSmem, s>>>(ctx->A, ctx->B, ctx->listB, nB, ctx->cat, ctx->sem,
                                                                  ctx->counts, c_rp, c_col, c_val, ctx->err);
+    ctx->end();
+    MG_CUDA(cudaGetLastError());
+  }
+  const int64_t nD = ctx->host_stats[mg::kStatND];
+  if (nD > 0) {
+    const int64_t blocks = (nD + mg::kDT / 32 - 1) / (mg::kDT / 32);
+    const unsigned grid = (unsigned)std::min<int64_t>(blocks, (int64_t)ctx->sm_count * 2 * 4);
+    ctx->begin(numeric ? MAGNUS_K_NUM_DENSE : MAGNUS_K_SYM_DENSE);
+    if (numeric)
+      mg::k_rows_dense<true><<<grid, mg::kDT, mg::DenseRowSmem::kTotal, s>>>(ctx->A, ctx->B, ctx->listD, nD, ctx->mn,
+                                                                           ctx->mx, ctx->counts, c_rp, c_col, c_val,
+                                                                           ctx->err);
+    else
+      mg::k_rows_dense<false><<<grid, mg::kDT, mg::DenseRowSmem::kTotal, s>>>(ctx->A, ctx->B, ctx->listD, nD, ctx->mn,
+                                                                            ctx->mx, ctx->counts, c_rp, c_col, c_val,
+                                                                            ctx->err);
     ctx->end();
     MG_CUDA(cudaGetLastError());
   }

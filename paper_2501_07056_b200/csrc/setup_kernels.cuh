@@ -55,14 +55,17 @@ struct CatParams {
 // stats layout (int64): [0..3] rows per category, [4] sum inter, [5] max nk of heavy rows,
 // [6] nW, [7] nB, [8] nH, [9] error flag, [10] n coarse rows
 constexpr int kStatCat = 0, kStatInter = 4, kStatMaxNk = 5, kStatNW = 6, kStatNB = 7, kStatNH = 8, kStatErr = 9,
-              kStatNCoarse = 10, kStatLen = 16;
+              kStatNCoarse = 10, kStatND = 11, kStatLen = 16;
+// dense-category rows handled warp-per-row without sorting (dense_rows.cuh)
+constexpr int64_t kDenseRangeMax = 32768, kDenseInterMax = 1024;
 
 // categorize_rows (reference magnus.py:68-94): first matching rule wins.
 // Also bins rows into the device execution classes and lists coarse rows.
 __global__ void k_categorize(int64_t n, DevCsr A, const int64_t* __restrict__ inter, const int64_t* __restrict__ mn,
                              const int64_t* __restrict__ mx, CatParams p, int8_t* __restrict__ cat,
                              int32_t* __restrict__ listW, int32_t* __restrict__ listB, int32_t* __restrict__ listH,
-                             int32_t* __restrict__ listCoarse, unsigned long long* __restrict__ stats) {
+                             int32_t* __restrict__ listCoarse, int32_t* __restrict__ listD,
+                             unsigned long long* __restrict__ stats) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = inter[i];
     const int64_t range = mx[i] - mn[i] + 1;
@@ -78,7 +81,9 @@ __global__ void k_categorize(int64_t n, DevCsr A, const int64_t* __restrict__ in
       listCoarse[slot] = (int32_t)i;
     }
     if (s == 0) continue;
-    if (s <= kWarpMax) {
+    if (c == kCatDense && range <= kDenseRangeMax && s <= kDenseInterMax) {
+      listD[atomicAdd(&stats[kStatND], 1ull)] = (int32_t)i;
+    } else if (s <= kWarpMax) {
       listW[atomicAdd(&stats[kStatNW], 1ull)] = (int32_t)i;
     } else if (s <= kBlockMax) {
       listB[atomicAdd(&stats[kStatNB], 1ull)] = (int32_t)i;
