@@ -18,6 +18,7 @@
 // processed in stream batches with a per-column carry (sequential association
 // only; windows containing pairwise columns are narrowed until they fit).
 #pragma once
+#include "binned_rows.cuh"
 #include "common.cuh"
 
 namespace mg {
@@ -181,18 +182,20 @@ __device__ __forceinline__ int kstate_find(const KState& st, int nk, uint32_t p)
 // each chunk's accumulator (accumulators.py:132-134), stored as mode bits.
 struct HeavySymSmem {
   static constexpr size_t kBitmap = (kSymWin / 32) * 4;                 // 128 KB
-  static constexpr size_t kChunk = kChunkSmem * 4;                       // 32 KB
+  static constexpr size_t kChunk = kChunkSmem * 4 * 2;                   // 64 KB: elements + distinct columns per chunk
   static constexpr size_t kK = (size_t)kKS * 4 * 5 + (kKS + 4) * 4 + kKS * 8;
   static constexpr size_t kScratch = 64 * 8;
   static constexpr size_t kTotal = kBitmap + kChunk + kK + kScratch;
   static_assert(kBitmap % 16 == 0 && kChunk % 16 == 0 && kK % 16 == 0, "16-byte aligned sections");
+  static_assert(kTotal + 64 <= 232448, "fits the opt-in shared memory of one CTA");
 };
 
 __global__ void __launch_bounds__(kHT, 1)
 k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows, const int8_t* __restrict__ cat,
                  const int64_t* __restrict__ mn, const int64_t* __restrict__ mx, Sem sem, int64_t* __restrict__ counts,
                  uint32_t* __restrict__ modebits, uint32_t* __restrict__ gk, int64_t gk_stride,
-                 uint32_t* __restrict__ gchunk, unsigned long long* __restrict__ work) {
+                 uint32_t* __restrict__ gchunk, unsigned long long* __restrict__ work, int binned, int64_t ncnt,
+                 const int64_t* __restrict__ choff, uint32_t* __restrict__ ce, uint32_t* __restrict__ cd) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem);
   uint32_t* ccnt_s = reinterpret_cast<uint32_t*>(smem + HeavySymSmem::kBitmap);
@@ -202,10 +205,14 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
   __shared__ int64_t s_row;
 
   for (int i = threadIdx.x; i < kSymWin / 32; i += kHT) bitmap[i] = 0;
-  for (int i = threadIdx.x; i < kChunkSmem; i += kHT) ccnt_s[i] = 0;
-  uint32_t* ccnt_g = gchunk + (size_t)blockIdx.x * (size_t)(sem.n_chunks_num);
-  const bool chunk_in_smem = sem.n_chunks_num <= kChunkSmem;
-  uint32_t* ccnt = chunk_in_smem ? ccnt_s : ccnt_g;
+  for (int i = threadIdx.x; i < 2 * kChunkSmem; i += kHT) ccnt_s[i] = 0;
+  // ncnt counters per array: numeric-plan chunks (mode bits), or column bins (binned numeric path)
+  uint32_t* ccnt_g = gchunk + (size_t)blockIdx.x * (size_t)ncnt * 2;
+  const bool chunk_in_smem = ncnt <= kChunkSmem;
+  uint32_t* ccnt = chunk_in_smem ? ccnt_s : ccnt_g;                      // elements per chunk / bin
+  uint32_t* dcnt = chunk_in_smem ? ccnt_s + kChunkSmem : ccnt_g + ncnt;  // distinct columns per bin
+  const int shift = binned ? bin_shift_of(sem.shift_num) : sem.shift_num;
+  const int wpc = shift >= 5 ? 1 << (shift - 5) : 1;   // bitmap words per bin (binned: windows are bin aligned)
   __syncthreads();
 
   while (true) {
@@ -236,9 +243,11 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
     }
     kstate_load<kHT>(st, A, B, a0, nk);
     const int ci = cat[i];
-    const bool need_modes = (ci == kCatFine || ci == kCatCoarse);
+    const bool need_modes = !binned && (ci == kCatFine || ci == kCatCoarse);
+    const bool need_counts = need_modes || binned;
     const int64_t row_lo = mn[i], row_hi = mx[i];
-    int64_t lo = row_lo;
+    const int64_t cmask = binned ? ~(((int64_t)1 << shift) - 1) : ~(int64_t)0;
+    int64_t lo = row_lo & cmask;
     uint64_t total = 0;
     __syncthreads();
     while (lo <= row_hi) {
@@ -256,7 +265,7 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
             const uint32_t c = __ldg(B.col + pos);
             const uint32_t lc = (uint32_t)(c - lo);
             atomicOr(&bitmap[lc >> 5], 1u << (lc & 31));
-            if (need_modes) atomicAdd(&ccnt[c >> sem.shift_num], 1u);
+            if (need_counts) atomicAdd(&ccnt[c >> shift], 1u);
           }
         }
       }
@@ -264,17 +273,51 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
       const int64_t width = (hi_all ? row_hi + 1 : hi) - lo;
       const int words = (int)((width + 31) >> 5);
       uint32_t pc = 0;
-      for (int wd = threadIdx.x; wd < words; wd += kHT) {
-        pc += __popc(bitmap[wd]);
-        bitmap[wd] = 0;
+      if (binned) {
+        // per-chunk distinct counts: one warp per chunk of the window
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        if (wpc <= 32) {
+          // a warp covers 32 consecutive words = 32 / wpc whole bins; segmented lane sums
+          for (int w0 = wid * 32; w0 < words; w0 += kHT) {
+            const int wd = w0 + lane;
+            uint32_t cp = 0;
+            if (wd < words) {
+              cp = __popc(bitmap[wd]);
+              bitmap[wd] = 0;
+            }
+            for (int o = wpc >> 1; o > 0; o >>= 1) cp += __shfl_xor_sync(0xffffffffu, cp, o);
+            if ((lane & (wpc - 1)) == 0 && cp) {
+              dcnt[(lo >> shift) + wd / wpc] += cp;
+              pc += cp;
+            }
+          }
+        } else {
+          const int nchw = (words + wpc - 1) / wpc;
+          for (int cj = wid; cj < nchw; cj += kHT / 32) {
+            uint32_t cp = 0;
+            for (int wd = cj * wpc + lane; wd < min(words, (cj + 1) * wpc); wd += 32) {
+              cp += __popc(bitmap[wd]);
+              bitmap[wd] = 0;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cp += __shfl_xor_sync(0xffffffffu, cp, o);
+            if (lane == 0 && cp) dcnt[(lo >> shift) + cj] += cp;
+            pc += lane == 0 ? cp : 0u;
+          }
+        }
+      } else {
+        for (int wd = threadIdx.x; wd < words; wd += kHT) {
+          pc += __popc(bitmap[wd]);
+          bitmap[wd] = 0;
+        }
       }
       total += block_sum<kHT>(pc, scratch);
       const int64_t nxt = kstate_advance<kHT>(st, B, nk, scratch64);
-      lo = nxt == INT64_MAX ? row_hi + 1 : nxt;
+      lo = nxt == INT64_MAX ? row_hi + 1 : (nxt & cmask);
     }
     if (threadIdx.x == 0) counts[i] = (int64_t)total;
+    const int64_t f0 = row_lo >> shift, f1 = row_hi >> shift;
     if (need_modes) {
-      const int64_t f0 = row_lo >> sem.shift_num, f1 = row_hi >> sem.shift_num;
       uint32_t* mb = modebits + (size_t)w * sem.mode_words;
       for (int64_t wd = (f0 >> 5) + threadIdx.x; wd <= (f1 >> 5); wd += kHT) {
         uint32_t bits = 0;
@@ -286,7 +329,25 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
         }
         mb[wd] = bits;
       }
-      __syncthreads();
+    }
+    __syncthreads();
+    if (binned) {
+      // chunk tables of this row: exclusive prefixes (buffer offsets / C offsets) + totals
+      const int nch = (int)(f1 - f0 + 1);
+      const int64_t eo = choff[w];
+      const uint32_t te = block_scan_striped<kHT>(ccnt + f0, nch, scratch);
+      const uint32_t td = block_scan_striped<kHT>(dcnt + f0, nch, scratch);
+      for (int j = threadIdx.x; j < nch; j += kHT) {
+        ce[eo + j] = ccnt[f0 + j];
+        cd[eo + j] = dcnt[f0 + j];
+        ccnt[f0 + j] = 0;
+        dcnt[f0 + j] = 0;
+      }
+      if (threadIdx.x == 0) {
+        ce[eo + nch] = te;
+        cd[eo + nch] = td;
+      }
+    } else if (need_modes) {
       for (int64_t f = f0 + threadIdx.x; f <= f1; f += kHT) ccnt[f] = 0;
     }
     __syncthreads();

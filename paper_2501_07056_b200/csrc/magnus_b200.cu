@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/magnus_b200.h"
+#include "binned_rows.cuh"
 #include "common.cuh"
 #include "dense_rows.cuh"
 #include "heavy_rows.cuh"
@@ -103,6 +104,17 @@ struct magnus_ctx {
   uint32_t* gk = nullptr;
   uint32_t* gchunk = nullptr;
   int64_t gk_stride = 0;
+  // binned heavy path (binned_rows.cuh)
+  bool binned = false;
+  int gshift = 0;        // column bin shift (bins nest in the numeric-plan chunks)
+  int64_t ncnt = 0;      // per-CTA chunk/bin counters of the heavy symbolic kernel
+  int64_t* choff = nullptr;   // per heavy row: first chunk-table entry (nH + 1)
+  int64_t* hbase = nullptr;   // per heavy row: exclusive prefix of the stream sizes (nH + 1)
+  int64_t* nent = nullptr;
+  int64_t* hinter = nullptr;
+  uint32_t* ce = nullptr;     // chunk tables: element prefix / distinct-column prefix
+  uint32_t* cd = nullptr;
+  std::vector<int64_t> h_hinter, h_nent;
   int64_t host_stats[mg::kStatLen] = {0};
   int64_t coarse_batches = 0;
   mg::Sem sem{};
@@ -219,6 +231,20 @@ int magnus_ctx_create(magnus_ctx** out) {
   auto* c = new magnus_ctx();
   MG_CUDA(cudaGetDevice(&c->device));
   MG_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
+  {
+    // keep freed workspace (reorder buffer, chunk tables) in the stream-ordered pool between
+    // calls instead of unmapping it at every synchronisation: up to a quarter of HBM
+    size_t fr = 0, tot = 0;
+    MG_CUDA(cudaMemGetInfo(&fr, &tot));
+    cudaMemPool_t pool;
+    MG_CUDA(cudaDeviceGetDefaultMemPool(&pool, c->device));
+    uint64_t thr = 0;
+    MG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    if (thr < tot / 4) {
+      thr = tot / 4;
+      MG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+  }
   MG_CUDA(cudaFuncSetAttribute(mg::k_rows_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mg::kBSmem));
   MG_CUDA(cudaFuncSetAttribute(mg::k_rows_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mg::kBSmem));
   MG_CUDA(cudaFuncSetAttribute(mg::k_rows_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -229,6 +255,11 @@ int magnus_ctx_create(magnus_ctx** out) {
                                (int)mg::HeavySymSmem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_heavy_numeric, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::HeavyNumSmem::kTotal));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_bin_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(mg::bin_reduce_warp_smem(mg::kBinMaxShift) * (mg::kBinT / 32))));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_bin_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)mg::bin_big_smem(mg::kBinMaxShift)));
+
   *out = c;
   return MAGNUS_OK;
 }
@@ -271,7 +302,7 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   if (th->sort_dense_crossover < 1 || th->sort_sweet_spot > th->sort_dense_crossover)
     return set_err(MAGNUS_INPUT, "invalid AccumThresholds");
   if (th->sort_dense_crossover > mg::kCap)
-    return set_err(MAGNUS_INPUT, "sort_dense_crossover above the device batch capacity (8192)");
+    return set_err(MAGNUS_INPUT, "sort_dense_crossover above the device batch capacity (" + std::to_string(mg::kCap) + ")");
   ctx->free_all();
   ctx->stream = (cudaStream_t)stream;
   cudaStream_t s = ctx->stream;
@@ -379,11 +410,41 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   const int64_t maxnk = ctx->host_stats[mg::kStatMaxNk];
   ctx->gk_stride = maxnk > mg::kKSN ? ((maxnk + 8) / 4) * 4 : 4;
   MG_CUDA(ctx->alloc(&ctx->gk, (size_t)2 * ctx->sm_count * ctx->gk_stride * 7));
-  const bool chunk_global = n_chunks_global > mg::kChunkSmem;
-  MG_CUDA(ctx->alloc(&ctx->gchunk, chunk_global ? (size_t)ctx->sm_count * n_chunks_global : 1));
-  if (chunk_global) MG_CUDA(cudaMemsetAsync(ctx->gchunk, 0, (size_t)ctx->sm_count * n_chunks_global * 4, s));
+  // binned heavy path: chunk width <= 2^14 and every big chunk dense (crossover <= kBinE)
+  ctx->binned = nH > 0 && ctx->sem.shift_num <= mg::kBinMaxShift && th->sort_dense_crossover <= mg::kBinE;
+  ctx->gshift = mg::bin_shift_of(ctx->sem.shift_num);
+  ctx->ncnt = ctx->binned ? (ctx->plan_num.plan_cols >> ctx->gshift) : n_chunks_global;
+  const bool chunk_global = ctx->ncnt > mg::kChunkSmem;
+  MG_CUDA(ctx->alloc(&ctx->gchunk, chunk_global ? (size_t)ctx->sm_count * ctx->ncnt * 2 : 1));
+  if (chunk_global) MG_CUDA(cudaMemsetAsync(ctx->gchunk, 0, (size_t)ctx->sm_count * ctx->ncnt * 8, s));
   MG_CUDA(ctx->alloc(&ctx->counts, n + 1));
   MG_CUDA(ctx->alloc(&ctx->tile_sums, (n + mg::kScanTile - 1) / mg::kScanTile + 1));
+  if (ctx->binned) {
+    MG_CUDA(ctx->alloc(&ctx->nent, nH));
+    MG_CUDA(ctx->alloc(&ctx->hinter, nH));
+    MG_CUDA(ctx->alloc(&ctx->choff, nH + 1));
+    MG_CUDA(ctx->alloc(&ctx->hbase, nH + 1));
+    mg::k_bin_prep<<<(unsigned)std::min<int64_t>((nH + 255) / 256, (int64_t)ctx->sm_count * 8), 256, 0, s>>>(
+        ctx->listH, nH, ctx->inter, ctx->mn, ctx->mx, ctx->gshift, ctx->nent, ctx->hinter);
+    const int64_t tiles = (nH + mg::kScanTile - 1) / mg::kScanTile;
+    mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->nent, nH, ctx->tile_sums);
+    mg::k_scan_tiles<<<1, 1024, 0, s>>>(ctx->tile_sums, tiles);
+    mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->nent, nH, ctx->tile_sums, ctx->choff);
+    mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->hinter, nH, ctx->tile_sums);
+    mg::k_scan_tiles<<<1, 1024, 0, s>>>(ctx->tile_sums, tiles);
+    mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->hinter, nH, ctx->tile_sums, ctx->hbase);
+    ctx->launches += 7;
+    MG_CUDA(cudaGetLastError());
+    ctx->h_hinter.resize(nH);
+    ctx->h_nent.resize(nH);
+    int64_t total_ent = 0;
+    MG_CUDA(cudaMemcpyAsync(ctx->h_hinter.data(), ctx->hinter, nH * 8, cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaMemcpyAsync(ctx->h_nent.data(), ctx->nent, nH * 8, cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaMemcpyAsync(&total_ent, ctx->choff + nH, 8, cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    MG_CUDA(ctx->alloc(&ctx->ce, total_ent));
+    MG_CUDA(ctx->alloc(&ctx->cd, total_ent));
+  }
   ctx->ready = true;
   return MAGNUS_OK;
 }
@@ -394,10 +455,118 @@ int magnus_categories(magnus_ctx* ctx, int8_t* dst, void* stream) {
   return MAGNUS_OK;
 }
 
+// Heavy rows, numeric phase, binned path: batches of rows whose products fit the reorder buffer.
+static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, double* c_val) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nH = ctx->host_stats[mg::kStatNH];
+  int64_t max_row = 0, total = 0;
+  for (int64_t h = 0; h < nH; ++h) {
+    max_row = std::max(max_row, ctx->h_hinter[h]);
+    total += ctx->h_hinter[h];
+  }
+  size_t free_b = 0, tot_b = 0;
+  MG_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+  {
+    // memory the pool holds but does not use is available too
+    cudaMemPool_t pool;
+    MG_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+    uint64_t reserved = 0, used = 0;
+    MG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+    MG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+    if (reserved > used) free_b += (size_t)(reserved - used);
+  }
+  const int64_t per_elem = 10;   // u16 local column + f64 product
+  int64_t cap = std::min<int64_t>(total, std::min<int64_t>((int64_t)(free_b * 0.4) / per_elem, int64_t(3) << 30));
+  cap = std::max(cap, max_row);
+  // batches [h0, h1) and the largest chunk-table span of a batch
+  std::vector<int64_t> cuts{0};
+  int64_t acc = 0, ent = 0, max_ent = 0;
+  for (int64_t h = 0; h < nH; ++h) {
+    if (acc + ctx->h_hinter[h] > cap && h > cuts.back()) {
+      cuts.push_back(h);
+      max_ent = std::max(max_ent, ent);
+      acc = ent = 0;
+    }
+    acc += ctx->h_hinter[h];
+    ent += ctx->h_nent[h];
+  }
+  cuts.push_back(nH);
+  max_ent = std::max(max_ent, ent);
+  int64_t buf_elems = 0;
+  {
+    int64_t a = 0;
+    for (size_t b = 0; b + 1 < cuts.size(); ++b, a = 0) {
+      for (int64_t h = cuts[b]; h < cuts[b + 1]; ++h) a += ctx->h_hinter[h];
+      buf_elems = std::max(buf_elems, a);
+    }
+  }
+  void *bcol = nullptr, *bval = nullptr, *items = nullptr, *cnts = nullptr;
+  MG_CUDA(cudaMallocAsync(&bcol, (size_t)std::max<int64_t>(buf_elems, 1) * 2, s));
+  MG_CUDA(cudaMallocAsync(&bval, (size_t)std::max<int64_t>(buf_elems, 1) * 8, s));
+  MG_CUDA(cudaMallocAsync(&items, (size_t)std::max<int64_t>(max_ent, 1) * 3 * sizeof(mg::BinItem), s));
+  MG_CUDA(cudaMallocAsync(&cnts, 64, s));
+  mg::BinItem* wins = static_cast<mg::BinItem*>(items);
+  mg::BinItem* units = wins + std::max<int64_t>(max_ent, 1);
+  mg::BinItem* bigs = units + std::max<int64_t>(max_ent, 1);
+  auto* nwin = static_cast<unsigned long long*>(cnts);
+  auto* nunit = nwin + 1;
+  auto* nbig = nwin + 2;
+  const size_t big_smem = mg::bin_big_smem(ctx->sem.shift_num);
+  int occ_b = 1;
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, mg::k_bin_big, mg::kBigT, big_smem));
+  const size_t red_smem = mg::bin_reduce_warp_smem(ctx->sem.shift_num) * (mg::kBinT / 32);
+  int occ = 1;
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mg::k_bin_reduce, mg::kBinT, red_smem));
+  int occ_e = 1;
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, mg::k_bin_expand, mg::kBinT, 0));
+  std::vector<int64_t> hb(cuts.size());
+  {
+    int64_t a = 0;
+    size_t b = 0;
+    for (int64_t h = 0; h <= nH; ++h) {
+      while (b < cuts.size() && cuts[b] == h) hb[b++] = a;
+      if (h < nH) a += ctx->h_hinter[h];
+    }
+  }
+  for (size_t b = 0; b + 1 < cuts.size(); ++b) {
+    const int64_t h0 = cuts[b], h1 = cuts[b + 1];
+    MG_CUDA(cudaMemsetAsync(cnts, 0, 64, s));
+    ctx->begin(MAGNUS_K_BIN_PLAN);
+    mg::k_bin_plan<<<(unsigned)std::min<int64_t>((h1 - h0 + 7) / 8, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+        ctx->listH, h0, h1, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, wins, nwin, bigs, nbig, units,
+        nunit);
+    ctx->end();
+    ctx->begin(MAGNUS_K_BIN_EXPAND);
+    mg::k_bin_expand<<<(unsigned)(ctx->sm_count * occ_e), mg::kBinT, 0, s>>>(
+        ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
+        nunit, nwin + 3, static_cast<uint16_t*>(bcol), static_cast<double*>(bval));
+    ctx->end();
+    ctx->begin(MAGNUS_K_BIN_REDUCE);
+    mg::k_bin_reduce<<<(unsigned)(ctx->sm_count * occ), mg::kBinT, red_smem, s>>>(
+        ctx->listH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->hbase, hb[b], wins, nwin,
+        nwin + 4, static_cast<const uint16_t*>(bcol), static_cast<const double*>(bval), c_rp, c_col, c_val, ctx->err);
+    ctx->end();
+    ctx->begin(MAGNUS_K_BIN_BIG);
+    mg::k_bin_big<<<(unsigned)(ctx->sm_count * occ_b), mg::kBigT, big_smem, s>>>(
+        ctx->listH, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->hbase, hb[b], bigs, nbig, nwin + 5,
+        static_cast<const uint16_t*>(bcol), static_cast<const double*>(bval), c_rp, c_col, c_val, ctx->err);
+    ctx->end();
+    MG_CUDA(cudaGetLastError());
+  }
+  MG_CUDA(cudaFreeAsync(bcol, s));
+  MG_CUDA(cudaFreeAsync(bval, s));
+  MG_CUDA(cudaFreeAsync(items, s));
+  MG_CUDA(cudaFreeAsync(cnts, s));
+  return MAGNUS_OK;
+}
+
 static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint32_t* c_col, double* c_val) {
   cudaStream_t s = ctx->stream;
   const int64_t nW = ctx->host_stats[mg::kStatNW], nB = ctx->host_stats[mg::kStatNB], nH = ctx->host_stats[mg::kStatNH];
-  if (nH > 0) {
+  if (nH > 0 && numeric && ctx->binned) {
+    int rc = launch_binned(ctx, c_rp, c_col, c_val);
+    if (rc) return rc;
+  } else if (nH > 0) {
     MG_CUDA(cudaMemsetAsync(ctx->work, 0, 8, s));
     const unsigned grid = (unsigned)std::min<int64_t>(nH, numeric ? 2 * ctx->sm_count : ctx->sm_count);
     ctx->begin(numeric ? MAGNUS_K_NUM_HEAVY : MAGNUS_K_SYM_HEAVY);
@@ -408,7 +577,7 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
     else
       mg::k_heavy_symbolic<<<grid, mg::kHT, mg::HeavySymSmem::kTotal, s>>>(
           ctx->A, ctx->B, ctx->listH, nH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->counts, ctx->modebits, ctx->gk,
-          ctx->gk_stride, ctx->gchunk, ctx->work);
+          ctx->gk_stride, ctx->gchunk, ctx->work, ctx->binned ? 1 : 0, ctx->ncnt, ctx->choff, ctx->ce, ctx->cd);
     ctx->end();
     MG_CUDA(cudaGetLastError());
   }

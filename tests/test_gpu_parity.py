@@ -124,3 +124,13 @@ def test_edge_shapes():
     assert r.C.n_rows == 0 and r.C.nnz == 0
     with pytest.raises(Exception):
         spgemm_magnus(F, F, sys=B200)   # 5x7 . 5x7: dimension mismatch -> InputError
+
+
+@pytest.mark.parametrize("crossover", [512, 1024, 3000])
+def test_heavy_paths_by_crossover(crossover):
+    """crossover <= 512 runs the binned heavy path, above it the windowed heavy kernel."""
+    th = AccumThresholds(sort_dense_crossover=crossover, sort_sweet_spot=8)
+    for A, B in (CASES["hub"](), CASES["rmat14"]()):
+        for sysp in (B200, FINE4K):
+            ref = oracle.spgemm(A, B, sysp, thresholds=th)
+            assert_same(spgemm_magnus(A, B, sys=sysp, thresholds=th), ref)
