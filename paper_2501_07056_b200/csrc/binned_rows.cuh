@@ -44,12 +44,20 @@ constexpr int kBinMaxShift = 14;      // chunk width <= 16384 columns (u16 chunk
 constexpr int kSubShift = 14;         // table granularity (sub-bin == chunk while shift_num <= 14)
 constexpr int kBinCur = 1024;         // expand: chunk cursors per warp (shared memory)
 constexpr int64_t kBinUnitMax = 1 << 18;   // expand: elements per unit (rows above are split by chunk ranges)
-constexpr int kBinU = 8;              // waves of loads in flight per lane
+#ifndef MG_EXP_U
+#define MG_EXP_U 8
+#endif
+#ifndef MG_EXP_MINB
+#define MG_EXP_MINB 8
+#endif
+constexpr int kBinU = MG_EXP_U;       // waves of loads in flight per lane
+constexpr uint32_t kBigSplit = 1u << 17;   // big chunks above this many elements are split by columns
+constexpr int kBigMaxParts = 32;
 
 __host__ __device__ inline int bin_shift_of(int shift_num) { return shift_num < kSubShift ? shift_num : kSubShift; }
 
 struct BinItem {   // table entries (sub-bins) [ja, jb) of heavy row h
-  int32_t h, ja, jb, kind;   // window: 0 = whole small chunks, 1 = one sub-bin of a big chunk; unit: 1 = whole row
+  int32_t h, ja, jb, kind;   // unit: 1 = whole row; big chunk: column part (kind & 0xffff) of (kind >> 16) parts
 };
 
 // shared memory of one reduce warp for chunk width 2^shift
@@ -143,7 +151,13 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
         emit_items(cut && !big && pi > __ldg(e + wjs), BinItem{(int32_t)h, wjs, je, 0}, wins, nwin);
         if (cm) wstart = q0 + 31 - __clz(cm) + 1;
       }
-      emit_items(big, BinItem{(int32_t)h, js, je, 1}, bigs, nbig);
+      // big chunks: one item, or column parts of ~kBigSplit elements each (every part
+      // streams the whole slice but applies only its own columns)
+      if (big) {
+        const int parts = (int)min((uint32_t)kBigMaxParts, (n + kBigSplit - 1) / kBigSplit);
+        const unsigned long long b0i = atomicAdd(nbig, (unsigned long long)parts);
+        for (int pp = 0; pp < parts; ++pp) bigs[b0i + pp] = BinItem{(int32_t)h, js, je, (parts << 16) | pp};
+      }
       // ---- expand units: chunk ranges (whole chunks, so small-chunk slices stay in one unit)
       const bool ucut = valid && (cj == rb.nchunk - 1 ||
                                   (split && (((cj + 1) % ucj) == 0 ||
@@ -161,7 +175,7 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
 }
 
 // Expand: one warp per unit; products appended to their slice in ascending k.
-__global__ void __launch_bounds__(kBinT)
+__global__ void __launch_bounds__(kBinT, MG_EXP_MINB)
 k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t* __restrict__ mn,
              const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce,
              const int64_t* __restrict__ hbase, int64_t batch_base, const BinItem* __restrict__ units,
@@ -207,8 +221,19 @@ k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t
     const int64_t chi64 = (rb.b0 + it.jb) << gs;
     const uint32_t chi = chi64 >= ((int64_t)1 << 32) ? 0xffffffffu : (uint32_t)chi64;
     __syncwarp();
-    // groups of 32 k's: the group's segments are flattened into one stream of positions
-    // (lane-consecutive), so loads of many short B rows are in flight together
+    // slice of column c (chunk, or sub-bin inside a big chunk), relative to the unit
+    auto slice_of = [&](uint32_t c) -> uint32_t {
+      const int64_t ck = c >> shift;
+      if (rb.cs == 0) return (uint32_t)(ck - rb.b0 - it.ja);
+      const int r = (int)(ck - cfirst);
+      const bool big = (bigm[r >> 5] >> (r & 31)) & 1u;
+      const int64_t ent = big ? (int64_t)(c >> gs) - rb.b0 : max((int64_t)0, (ck << rb.cs) - rb.b0);
+      return (uint32_t)(ent - it.ja);
+    };
+    // groups of 32 k's, in order.  A long B row (>= 32 products) is walked on its own,
+    // 32 consecutive products per wave (equal slices are contiguous runs); a run of
+    // short B rows is flattened into one stream (lane-consecutive positions), so the
+    // loads of many short rows are in flight together.
     for (int64_t t0 = a0; t0 < a1; t0 += 32) {
       const int64_t t = t0 + lane;
       uint32_t p0 = 0, p1 = 0;
@@ -224,69 +249,104 @@ k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t
         }
       }
       const uint32_t len = p1 - p0;
-      const uint32_t inc = warp_incl_scan(len);
-      const uint32_t off = inc - len;
-      const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-      for (uint32_t q0 = 0; q0 < total; q0 += 32 * kBinU) {
-        uint32_t c[kBinU], tk[kBinU];
-        double v[kBinU];
+      const uint32_t longm = __ballot_sync(0xffffffffu, len >= 32u);
+      int ts = 0;
+      while (ts < 32) {
+        if ((longm >> ts) & 1u) {
+          // ---- one long B row
+          const uint32_t bb0 = __shfl_sync(0xffffffffu, p0, ts), bb1 = __shfl_sync(0xffffffffu, p1, ts);
+          const double a = __shfl_sync(0xffffffffu, av, ts);
+          for (uint32_t q0 = bb0; q0 < bb1; q0 += 32 * kBinU) {
+            uint32_t c[kBinU];
+            double v[kBinU];
 #pragma unroll
-        for (int w = 0; w < kBinU; ++w) {
-          const uint32_t q = q0 + w * 32 + lane;
-          // segment of stream position q: last lane with off <= q
-          int lo = 0;
-#pragma unroll
-          for (int st = 16; st > 0; st >>= 1) {
-            const uint32_t o = __shfl_sync(0xffffffffu, off, lo + st);
-            if (o <= q) lo += st;
-          }
-          const uint32_t pp = __shfl_sync(0xffffffffu, p0, lo) + (q - __shfl_sync(0xffffffffu, off, lo));
-          const double a = __shfl_sync(0xffffffffu, av, lo);
-          tk[w] = (uint32_t)lo;
-          c[w] = 0xffffffffu;
-          v[w] = 0.0;
-          if (q < total) {
-            c[w] = __ldg(B.col + pp);
-            v[w] = __dmul_rn(a, __ldg(B.val + pp));
-          }
-        }
-#pragma unroll
-        for (int w = 0; w < kBinU; ++w) {
-          if (q0 + w * 32 < total) {
-            const bool valid = c[w] != 0xffffffffu;
-            uint32_t fl = 0x80000000u | lane;   // unique for invalid lanes
-            if (valid) {
-              const int64_t ck = c[w] >> shift;
-              const int r = (int)(ck - cfirst);
-              const bool big = (bigm[r >> 5] >> (r & 31)) & 1u;
-              const int64_t ent = big ? (int64_t)(c[w] >> gs) - rb.b0 : max((int64_t)0, (ck << rb.cs) - rb.b0);
-              fl = (uint32_t)(ent - it.ja);
+            for (int w = 0; w < kBinU; ++w) {
+              const uint32_t pp = q0 + w * 32 + lane;
+              c[w] = 0xffffffffu;
+              v[w] = 0.0;
+              if (pp < bb1) {
+                c[w] = __ldg(B.col + pp);
+                v[w] = __dmul_rn(a, __ldg(B.val + pp));
+              }
             }
-            uint32_t rank, last;
-            const uint32_t t_first = __shfl_sync(0xffffffffu, tk[w], 0);
-            if (__all_sync(0xffffffffu, !valid || tk[w] == t_first)) {
-              // one B row: equal slices are contiguous runs
-              const uint32_t prevf = __shfl_up_sync(0xffffffffu, fl, 1);
-              const uint32_t nextf = __shfl_down_sync(0xffffffffu, fl, 1);
-              const uint32_t hm = __ballot_sync(0xffffffffu, lane == 0 || prevf != fl);
-              rank = (uint32_t)(lane - (31 - __clz(hm & lanemask_le())));
-              last = lane == 31 || nextf != fl;
-            } else {
+#pragma unroll
+            for (int w = 0; w < kBinU; ++w) {
+              if (q0 + w * 32 < bb1) {
+                const bool valid = c[w] != 0xffffffffu;
+                const uint32_t fl = valid ? slice_of(c[w]) : (0x80000000u | lane);
+                const uint32_t prevf = __shfl_up_sync(0xffffffffu, fl, 1);
+                const uint32_t nextf = __shfl_down_sync(0xffffffffu, fl, 1);
+                const uint32_t hm = __ballot_sync(0xffffffffu, lane == 0 || prevf != fl);
+                const uint32_t rank = (uint32_t)(lane - (31 - __clz(hm & lanemask_le())));
+                const bool last = lane == 31 || nextf != fl;
+                uint32_t slot = 0;
+                if (valid) slot = cur[fl] + rank;
+                __syncwarp();
+                if (valid && last) cur[fl] = slot + 1;
+                if (valid) {
+                  rc[slot] = (uint16_t)(c[w] & cmask);
+                  rv[slot] = v[w];
+                }
+                __syncwarp();
+              }
+            }
+          }
+          ++ts;
+          continue;
+        }
+        // ---- run of short B rows [ts, te): flattened
+        const uint32_t after = longm & ~((2u << ts) - 1u) & ~(ts == 31 ? 0xffffffffu : 0u);
+        const int te = after ? __ffs(after) - 1 : 32;
+        const uint32_t lr = (lane >= ts && lane < te) ? len : 0u;
+        const uint32_t inc = warp_incl_scan(lr);
+        const uint32_t off = inc - lr;
+        const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+        for (uint32_t q0 = 0; q0 < total; q0 += 32 * kBinU) {
+          uint32_t c[kBinU], tk[kBinU];
+          double v[kBinU];
+#pragma unroll
+          for (int w = 0; w < kBinU; ++w) {
+            const uint32_t q = q0 + w * 32 + lane;
+            // segment of stream position q: last lane with off <= q (lanes outside the run have
+            // lr = 0, so the search lands on a lane of the run)
+            int lo = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+              const uint32_t o = __shfl_sync(0xffffffffu, off, lo + st);
+              if (o <= q) lo += st;
+            }
+            const uint32_t pp = __shfl_sync(0xffffffffu, p0, lo) + (q - __shfl_sync(0xffffffffu, off, lo));
+            const double a = __shfl_sync(0xffffffffu, av, lo);
+            tk[w] = (uint32_t)lo;
+            c[w] = 0xffffffffu;
+            v[w] = 0.0;
+            if (q < total) {
+              c[w] = __ldg(B.col + pp);
+              v[w] = __dmul_rn(a, __ldg(B.val + pp));
+            }
+          }
+#pragma unroll
+          for (int w = 0; w < kBinU; ++w) {
+            if (q0 + w * 32 < total) {
+              const bool valid = c[w] != 0xffffffffu;
+              const uint32_t fl = valid ? slice_of(c[w]) : (0x80000000u | lane);
               const uint32_t peers = __match_any_sync(0xffffffffu, fl);
-              rank = __popc(peers & lanemask_lt());
-              last = (peers >> lane) == 1u;
+              const uint32_t rank = __popc(peers & lanemask_lt());
+              const bool last = (peers >> lane) == 1u;
+              (void)tk;
+              uint32_t slot = 0;
+              if (valid) slot = cur[fl] + rank;
+              __syncwarp();
+              if (valid && last) cur[fl] = slot + 1;
+              if (valid) {
+                rc[slot] = (uint16_t)(c[w] & cmask);
+                rv[slot] = v[w];
+              }
+              __syncwarp();
             }
-            uint32_t slot = 0;
-            if (valid) slot = cur[fl] + rank;
-            __syncwarp();
-            if (valid && last) cur[fl] = slot + 1;
-            if (valid) {
-              rc[slot] = (uint16_t)(c[w] & cmask);
-              rv[slot] = v[w];
-            }
-            __syncwarp();
           }
         }
+        ts = te;
       }
     }
     __syncwarp();
@@ -430,80 +490,8 @@ __device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* __restrict__ s
   return true;
 }
 
-// One sub-bin of a big chunk (dense association): stream-order accumulation into a dense
-// shared-memory window of the sub-bin's columns.  Inside one wave, lanes of the same
-// column are added by the lowest of them, in lane order.
-__device__ __forceinline__ bool reduce_bin_dense(const uint16_t* __restrict__ sc, const double* __restrict__ sv_g,
-                                                 uint32_t n, uint32_t m, int gs, uint32_t colbase, const ReduceSmem& S,
-                                                 uint32_t* __restrict__ c_col, double* __restrict__ c_val, int64_t out) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t bw = 1u << gs, bmask = bw - 1u;
-  const int nwords = (int)((bw + 31) >> 5);
-  double* acc = S.sval;
-  for (int wd = lane; wd < nwords; wd += 32) S.bm[wd] = 0u;
-  for (uint32_t c = lane; c < bw; c += 32) acc[c] = 0.0;
-  __syncwarp();
-  for (uint32_t q0 = 0; q0 < n; q0 += 32 * kBinU) {
-    uint32_t cc[kBinU];
-    double vv[kBinU];
-#pragma unroll
-    for (int w = 0; w < kBinU; ++w) {
-      const uint32_t q = q0 + w * 32 + lane;
-      cc[w] = 0x10000u + lane;
-      vv[w] = 0.0;
-      if (q < n) {
-        cc[w] = __ldg(sc + q) & bmask;
-        vv[w] = __ldg(sv_g + q);
-      }
-    }
-#pragma unroll
-    for (int w = 0; w < kBinU; ++w) {
-      if (q0 + w * 32 < n) {
-        const uint32_t c = cc[w];
-        const bool valid = c < 0x10000u;
-        const uint32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
-        const uint32_t brk = __ballot_sync(0xffffffffu, valid && lane > 0 && c <= pc);
-        if (valid) atomicOr(&S.bm[c >> 5], 1u << (c & 31));
-        if (!brk) {
-          if (valid) acc[c] = __dadd_rn(acc[c], vv[w]);
-        } else {
-          const uint32_t peers = __match_any_sync(0xffffffffu, c);
-          const uint32_t gsz = __popc(peers);
-          const uint32_t maxg = __reduce_max_sync(0xffffffffu, valid ? gsz : 0u);
-          const bool lead = valid && (peers & lanemask_lt()) == 0u;
-          double s = lead ? acc[c] : 0.0;
-          uint32_t rem = peers;
-          for (uint32_t k = 0; k < maxg; ++k) {
-            const int src = rem ? __ffs(rem) - 1 : lane;
-            if (rem) rem &= rem - 1u;
-            const double x = __shfl_sync(0xffffffffu, vv[w], src);
-            if (lead && k < gsz) s = __dadd_rn(s, x);
-          }
-          if (lead) acc[c] = s;
-        }
-        __syncwarp();
-      }
-    }
-  }
-  if (prefix_words(S.bm, S.pref, 0, nwords) != m) return false;
-  for (int wd = lane; wd < nwords; wd += 32) {
-    uint32_t bits = S.bm[wd];
-    uint32_t r = S.pref[wd];
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1u;
-      const uint32_t c = (uint32_t)(wd * 32 + b);
-      c_col[out + r] = colbase + c;
-      c_val[out + r] = acc[c];
-      ++r;
-    }
-  }
-  __syncwarp();
-  return true;
-}
-
 // Reduce: one warp per window.
-__global__ void __launch_bounds__(kBinT)
+__global__ void __launch_bounds__(kBinT, 8)
 k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, const int64_t* __restrict__ mn,
              const int64_t* __restrict__ mx, Sem sem, const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce,
              const uint32_t* __restrict__ cd, const int64_t* __restrict__ hbase, int64_t batch_base,
@@ -538,47 +526,43 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
     const int64_t rowbase = hbase[it.h] - batch_base;
     const int64_t out_row = c_rp[i];
     bool ok = true;
-    if (it.kind == 1) {
-      const int j = it.ja;
-      const uint32_t ej = __ldg(e + j), dj = __ldg(d + j);
-      ok = reduce_bin_dense(bcol + rowbase + ej, bval + rowbase + ej, __ldg(e + j + 1) - ej, __ldg(d + j + 1) - dj, gs,
-                            (uint32_t)((rb.b0 + j) << gs), S, c_col, c_val, out_row + dj);
-    } else {
-      int j = it.ja;
-      while (j < it.jb) {
-        const int je = (int)min((int64_t)it.jb, ((((rb.b0 + j) >> rb.cs) + 1) << rb.cs) - rb.b0);
-        const uint32_t ej = __ldg(e + j), n = __ldg(e + je) - ej;
-        if (n) {
-          const uint32_t dj = __ldg(d + j);
-          const bool seq = ci == kCatDense || (int64_t)n >= sem.crossover;
-          ok &= reduce_chunk_sort(bcol + rowbase + ej, bval + rowbase + ej, n, __ldg(d + je) - dj, seq,
-                                  (uint32_t)((rb.b0 + j) << gs) & cwmask, S, c_col, c_val, out_row + dj);
-        }
-        j = je;
+    int j = it.ja;
+    while (j < it.jb) {
+      const int je = (int)min((int64_t)it.jb, ((((rb.b0 + j) >> rb.cs) + 1) << rb.cs) - rb.b0);
+      const uint32_t ej = __ldg(e + j), n = __ldg(e + je) - ej;
+      if (n) {
+        const uint32_t dj = __ldg(d + j);
+        const bool seq = ci == kCatDense || (int64_t)n >= sem.crossover;
+        ok &= reduce_chunk_sort(bcol + rowbase + ej, bval + rowbase + ej, n, __ldg(d + je) - dj, seq,
+                                (uint32_t)((rb.b0 + j) << gs) & cwmask, S, c_col, c_val, out_row + dj);
       }
+      j = je;
     }
     if (!ok && (threadIdx.x & 31) == 0) atomicOr(err, 4ull);
   }
 }
 
 
-// Big chunk (> kBinE elements, dense association): one CTA per chunk, a dense
-// shared-memory window over the chunk's columns.  Columns are dealt to the 8 warps
-// in 16-column granules; the slice is taken in batches of kBigS elements: each warp
-// ranks its part of the batch by owner (ballots), a CTA scan turns the counts into
-// offsets, the batch is stably partitioned by owner into shared memory, and each
-// warp then applies its own elements in stream order -- a column is only ever
-// updated by its owner, in ascending k.
-constexpr int kBigT = 256;
-constexpr int kBigS = 2048;                 // elements per batch
-constexpr int kBigWaves = kBigS / kBigT;    // waves of 32 per warp per batch (8)
+// Big chunk (> kBinE elements, always the dense association): one warp per chunk.
+// The chunk's columns are marked in a bitmap and ranked (word prefix + popcount);
+// the products are then applied in stream order (ascending k) to a dense
+// shared-memory accumulator indexed by rank, kBigD ranks per pass (as the
+// reference's dense accumulator, accumulators.py:68-97).  Inside one wave the
+// lanes of a repeated column are added by the lowest of them, in lane order.
+// Loads run kBigU waves ahead.  Chunks above kBigSplit elements are split into
+// column parts handled by different warps.
+constexpr int kBigU = 8;
+#ifndef MG_BIG_D
+#define MG_BIG_D 2048
+#endif
+constexpr int kBigD = MG_BIG_D;   // ranks accumulated per pass (16 KB)
 
 __host__ __device__ inline size_t bin_big_smem(int shift) {
   const size_t width = size_t(1) << shift, words = (width + 31) / 32;
-  return width * 8 + ((words * 4 + 15) & ~size_t(15)) + (size_t)kBigS * 8 + (size_t)kBigS * 2 + 80 * 4;
+  return (size_t)kBigD * 8 + ((words * 4 + 15) & ~size_t(15)) + ((words * 2 + 15) & ~size_t(15));
 }
 
-__global__ void __launch_bounds__(kBigT)
+__global__ void __launch_bounds__(32)
 k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, const int64_t* __restrict__ mx, Sem sem,
           const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce, const uint32_t* __restrict__ cd,
           const int64_t* __restrict__ hbase, int64_t batch_base, const BinItem* __restrict__ bigs,
@@ -586,28 +570,19 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
           const uint16_t* __restrict__ bcol, const double* __restrict__ bval, const int64_t* __restrict__ c_rp,
           uint32_t* __restrict__ c_col, double* __restrict__ c_val, unsigned long long* __restrict__ err) {
   extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int NW = kBigT / 32;
-  static_assert(NW == 8, "8 owner warps");
   const int shift = sem.shift_num;
   const uint32_t width = 1u << shift;
   const int nwords = (int)((width + 31) / 32);
   double* acc = reinterpret_cast<double*>(smem);
-  unsigned char* p = smem + (size_t)width * 8;
-  uint32_t* bm = reinterpret_cast<uint32_t*>(p);
-  p += ((size_t)nwords * 4 + 15) & ~size_t(15);
-  double* stv = reinterpret_cast<double*>(p);
-  p += (size_t)kBigS * 8;
-  uint16_t* stc = reinterpret_cast<uint16_t*>(p);
-  p += (size_t)kBigS * 2;
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(p);   // [owner * NW + warp], then [64] = total
-  __shared__ unsigned long long s_item;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* bm = reinterpret_cast<uint32_t*>(smem + (size_t)kBigD * 8);
+  uint16_t* pref = reinterpret_cast<uint16_t*>(smem + (size_t)kBigD * 8 + (((size_t)nwords * 4 + 15) & ~size_t(15)));
+  const int lane = threadIdx.x & 31;
   const int64_t nbg = (int64_t)*nbig;
   while (true) {
-    if (threadIdx.x == 0) s_item = atomicAdd(ticket, 1ull);
-    __syncthreads();
-    const int64_t bi = (int64_t)s_item;
-    if (bi >= nbg) break;
+    unsigned long long bi = 0;
+    if (lane == 0) bi = atomicAdd(ticket, 1ull);
+    bi = __shfl_sync(0xffffffffu, bi, 0);
+    if ((int64_t)bi >= nbg) break;
     const BinItem it = bigs[bi];
     const int64_t i = rows[it.h];
     const RowBins rb = row_bins(mn[i], mx[i], shift);
@@ -620,115 +595,107 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
     const double* sv = bval + rowbase + ej;
     const int64_t out = c_rp[i] + dj;
     const uint32_t colbase = (uint32_t)(((rb.b0 + it.ja) >> rb.cs) << shift);
-    for (uint32_t c = threadIdx.x; c < width; c += kBigT) acc[c] = 0.0;
-    for (int wd = threadIdx.x; wd < nwords; wd += kBigT) bm[wd] = 0u;
-    __syncthreads();
-    for (uint32_t B0 = 0; B0 < n; B0 += kBigS) {
-      const uint32_t nb = min((uint32_t)kBigS, n - B0);
-      uint32_t cc[kBigWaves], off[kBigWaves];
-      double vv[kBigWaves];
+    const uint32_t parts = (uint32_t)it.kind >> 16, part = (uint32_t)it.kind & 0xffffu;
+    const uint32_t plo = (uint32_t)(((uint64_t)width * part) / parts), phi = (uint32_t)(((uint64_t)width * (part + 1)) / parts);
+    // ---- columns of the chunk -> ranks
+    for (int wd = lane; wd < nwords; wd += 32) bm[wd] = 0u;
+    __syncwarp();
+    for (uint32_t q0 = 0; q0 < n; q0 += 32 * kBigU) {
+      uint32_t cc[kBigU];
 #pragma unroll
-      for (int v = 0; v < kBigWaves; ++v) {
-        const uint32_t q = (uint32_t)wid * (kBigS / NW) + v * 32 + lane;
-        cc[v] = 0xffffffffu;
-        vv[v] = 0.0;
-        if (q < nb) {
-          cc[v] = __ldg(sc + B0 + q);
-          vv[v] = __ldg(sv + B0 + q);
-        }
+      for (int w = 0; w < kBigU; ++w) {
+        const uint32_t q = q0 + w * 32 + lane;
+        cc[w] = q < n ? (uint32_t)__ldg(sc + q) : 0xffffffffu;
       }
-      uint32_t run_cnt = 0;   // lane l < 8: this warp's elements owned by warp l so far
 #pragma unroll
-      for (int v = 0; v < kBigWaves; ++v) {
-        const bool valid = cc[v] != 0xffffffffu;
-        const uint32_t ow = valid ? (cc[v] >> 4) & 7u : 0u;
-        const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-        const uint32_t x0 = __ballot_sync(0xffffffffu, ow & 1u), x1 = __ballot_sync(0xffffffffu, ow & 2u),
-                       x2 = __ballot_sync(0xffffffffu, ow & 4u);
-        const uint32_t peers = vm & ((ow & 1u) ? x0 : ~x0) & ((ow & 2u) ? x1 : ~x1) & ((ow & 4u) ? x2 : ~x2);
-        const uint32_t mine_l = vm & ((lane & 1) ? x0 : ~x0) & ((lane & 2) ? x1 : ~x1) & ((lane & 4) ? x2 : ~x2);
-        off[v] = __shfl_sync(0xffffffffu, run_cnt, ow) + __popc(peers & lanemask_lt());
-        if (lane < NW) run_cnt += __popc(mine_l);
-      }
-      if (lane < NW) cnt[lane * NW + wid] = run_cnt;
-      __syncthreads();
-      if (wid == 0) {
-        const uint32_t a0 = cnt[2 * lane], a1 = cnt[2 * lane + 1];
-        const uint32_t inc = warp_incl_scan(a0 + a1);
-        const uint32_t ex = inc - a0 - a1;
-        cnt[2 * lane] = ex;
-        cnt[2 * lane + 1] = ex + a0;
-        if (lane == 31) cnt[64] = inc;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int v = 0; v < kBigWaves; ++v) {
-        if (cc[v] != 0xffffffffu) {
-          const uint32_t pos = cnt[((cc[v] >> 4) & 7u) * NW + wid] + off[v];
-          stc[pos] = (uint16_t)cc[v];
-          stv[pos] = vv[v];
-        }
-      }
-      __syncthreads();
-      const uint32_t lo = cnt[wid * NW], hi = wid == NW - 1 ? cnt[64] : cnt[(wid + 1) * NW];
-      for (uint32_t p0 = lo; p0 < hi; p0 += 32) {
-        const uint32_t q = p0 + lane;
-        const bool valid = q < hi;
-        const uint32_t c = valid ? (uint32_t)stc[q] : 0x10000u + lane;
-        const double v = valid ? stv[q] : 0.0;
-        const uint32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
-        const uint32_t brk = __ballot_sync(0xffffffffu, valid && lane > 0 && c <= pc);
-        if (valid) atomicOr(&bm[c >> 5], 1u << (c & 31));
-        if (!brk) {
-          if (valid) acc[c] = __dadd_rn(acc[c], v);
-        } else {
-          // ascending runs one after another (a column repeats only across runs)
-          const int run = __popc(brk & lanemask_le());
-          const int nruns = __popc(brk) + 1;
-          for (int rr = 0; rr < nruns; ++rr) {
-            if (valid && run == rr) acc[c] = __dadd_rn(acc[c], v);
-            __syncwarp();
-          }
-        }
-        __syncwarp();
-      }
-      __syncthreads();
+      for (int w = 0; w < kBigU; ++w)
+        if (cc[w] != 0xffffffffu) atomicOr(&bm[cc[w] >> 5], 1u << (cc[w] & 31));
     }
-    // compact: word prefix over the whole window (block scan), then write the touched columns
-    const uint32_t wpt = (nwords + kBigT - 1) / kBigT;   // words per thread (contiguous)
-    uint32_t cntw = 0;
-    for (uint32_t q = 0; q < wpt; ++q) {
-      const uint32_t wd = threadIdx.x * wpt + q;
-      if (wd < (uint32_t)nwords) cntw += __popc(bm[wd]);
+    __syncwarp();
+    if (prefix_words(bm, pref, 0, nwords) != m) {
+      if (lane == 0) atomicOr(err, 4ull);
+      continue;
     }
-    const uint32_t inc = warp_incl_scan(cntw);
-    if (lane == 31) cnt[wid] = inc;
-    __syncthreads();
-    if (wid == 0) {
-      const uint32_t wv = lane < NW ? cnt[lane] : 0u;
-      const uint32_t wi = warp_incl_scan(wv);
-      if (lane < NW) cnt[lane] = wi - wv;
-      if (lane == NW - 1) cnt[64] = wi;
-    }
-    __syncthreads();
-    uint32_t r = cnt[wid] + inc - cntw;
-    if (threadIdx.x == 0 && cnt[64] != m) atomicOr(err, 4ull);
-    for (uint32_t q = 0; q < wpt; ++q) {
-      const uint32_t wd = threadIdx.x * wpt + q;
-      if (wd >= (uint32_t)nwords) break;
+    const uint32_t rlo0 = plo < width ? rank_of(bm, pref, plo) : m;
+    const uint32_t rhi0 = phi < width ? rank_of(bm, pref, phi) : m;
+    // ---- columns of this part, ascending
+    for (int wd = (int)(plo >> 5) + lane; wd < (int)((phi + 31) >> 5); wd += 32) {
       uint32_t bits = bm[wd];
+      const uint32_t lo_b = wd * 32u < plo ? plo - wd * 32u : 0u, hi_b = phi - wd * 32u;
+      if (lo_b) bits &= ~((1u << lo_b) - 1u);
+      if (hi_b < 32u) bits &= (1u << hi_b) - 1u;
+      uint32_t r = pref[wd] + __popc(bm[wd] & (lo_b ? (1u << lo_b) - 1u : 0u));
       while (bits) {
         const int b = __ffs(bits) - 1;
         bits &= bits - 1u;
-        const uint32_t c = wd * 32 + b;
-        if (r < m) {
-          c_col[out + r] = colbase + c;
-          c_val[out + r] = acc[c];
-        }
+        c_col[out + r] = colbase + (uint32_t)(wd * 32 + b);
         ++r;
       }
     }
-    __syncthreads();
+    // ---- sums, kBigD ranks per pass; loads of the next kBigU waves in flight
+    for (uint32_t rlo = rlo0; rlo < rhi0; rlo += kBigD) {
+      const uint32_t rhi = min(rhi0, rlo + kBigD);
+      for (uint32_t r = lane; r < rhi - rlo; r += 32) acc[r] = 0.0;
+      __syncwarp();
+      uint32_t cc[kBigU], cn[kBigU];
+      double vv[kBigU], vn[kBigU];
+#pragma unroll
+      for (int w = 0; w < kBigU; ++w) {
+        const uint32_t q = w * 32 + lane;
+        cc[w] = q < n ? (uint32_t)__ldg(sc + q) : 0xffffffffu;
+        vv[w] = q < n ? __ldg(sv + q) : 0.0;
+      }
+      for (uint32_t q0 = 0; q0 < n; q0 += 32 * kBigU) {
+        const uint32_t q1 = q0 + 32 * kBigU;
+#pragma unroll
+        for (int w = 0; w < kBigU; ++w) {
+          const uint32_t q = q1 + w * 32 + lane;
+          cn[w] = q < n ? (uint32_t)__ldg(sc + q) : 0xffffffffu;
+          vn[w] = q < n ? __ldg(sv + q) : 0.0;
+        }
+        // ranks of all waves first (independent shared-memory loads), then the ordered updates
+        uint32_t rr[kBigU];
+#pragma unroll
+        for (int w = 0; w < kBigU; ++w) rr[w] = cc[w] != 0xffffffffu ? rank_of(bm, pref, cc[w]) : 0xffffffffu;
+#pragma unroll
+        for (int w = 0; w < kBigU; ++w) {
+          if (q0 + w * 32 < n) {
+            const double v = vv[w];
+            const uint32_t r = rr[w];
+            const bool valid = r >= rlo && r < rhi;
+            const uint32_t key = valid ? r - rlo : 0x10000u + lane;
+            const uint32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
+            const uint32_t brk = __ballot_sync(0xffffffffu, valid && lane > 0 && key <= pk);
+            if (!brk) {
+              if (valid) acc[key] = __dadd_rn(acc[key], v);
+            } else {
+              const uint32_t peers = __match_any_sync(0xffffffffu, key);
+              const uint32_t gsz = __popc(peers);
+              const uint32_t maxg = __reduce_max_sync(0xffffffffu, valid ? gsz : 0u);
+              const bool lead = valid && (peers & lanemask_lt()) == 0u;
+              double sacc = lead ? acc[key] : 0.0;
+              uint32_t rem = peers;
+              for (uint32_t k = 0; k < maxg; ++k) {
+                const int src = rem ? __ffs(rem) - 1 : lane;
+                if (rem) rem &= rem - 1u;
+                const double x = __shfl_sync(0xffffffffu, v, src);
+                if (lead && k < gsz) sacc = __dadd_rn(sacc, x);
+              }
+              if (lead) acc[key] = sacc;
+            }
+            __syncwarp();
+          }
+        }
+#pragma unroll
+        for (int w = 0; w < kBigU; ++w) {
+          cc[w] = cn[w];
+          vv[w] = vn[w];
+        }
+      }
+      __syncwarp();
+      for (uint32_t r = rlo + lane; r < rhi; r += 32) c_val[out + r] = acc[r - rlo];
+      __syncwarp();
+    }
   }
 }
 

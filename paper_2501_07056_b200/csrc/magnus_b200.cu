@@ -115,6 +115,8 @@ struct magnus_ctx {
   uint32_t* ce = nullptr;     // chunk tables: element prefix / distinct-column prefix
   uint32_t* cd = nullptr;
   std::vector<int64_t> h_hinter, h_nent;
+  cudaStream_t aux = nullptr;   // second stream for independent reducers
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int64_t host_stats[mg::kStatLen] = {0};
   int64_t coarse_batches = 0;
   mg::Sem sem{};
@@ -260,6 +262,9 @@ int magnus_ctx_create(magnus_ctx** out) {
   MG_CUDA(cudaFuncSetAttribute(mg::k_bin_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::bin_big_smem(mg::kBinMaxShift)));
 
+  MG_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+  MG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  MG_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   *out = c;
   return MAGNUS_OK;
 }
@@ -270,6 +275,9 @@ void magnus_ctx_destroy(magnus_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto& m : ctx->marks) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
 }
 
@@ -503,7 +511,9 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   void *bcol = nullptr, *bval = nullptr, *items = nullptr, *cnts = nullptr;
   MG_CUDA(cudaMallocAsync(&bcol, (size_t)std::max<int64_t>(buf_elems, 1) * 2, s));
   MG_CUDA(cudaMallocAsync(&bval, (size_t)std::max<int64_t>(buf_elems, 1) * 8, s));
-  MG_CUDA(cudaMallocAsync(&items, (size_t)std::max<int64_t>(max_ent, 1) * 3 * sizeof(mg::BinItem), s));
+  // windows and units: <= one per chunk entry; big-chunk parts: <= entries + elements / kBigSplit
+  const int64_t max_big = std::max<int64_t>(max_ent, 1) + buf_elems / mg::kBigSplit + 1;
+  MG_CUDA(cudaMallocAsync(&items, ((size_t)std::max<int64_t>(max_ent, 1) * 2 + (size_t)max_big) * sizeof(mg::BinItem), s));
   MG_CUDA(cudaMallocAsync(&cnts, 64, s));
   mg::BinItem* wins = static_cast<mg::BinItem*>(items);
   mg::BinItem* units = wins + std::max<int64_t>(max_ent, 1);
@@ -513,7 +523,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   auto* nbig = nwin + 2;
   const size_t big_smem = mg::bin_big_smem(ctx->sem.shift_num);
   int occ_b = 1;
-  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, mg::k_bin_big, mg::kBigT, big_smem));
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, mg::k_bin_big, 32, big_smem));
   const size_t red_smem = mg::bin_reduce_warp_smem(ctx->sem.shift_num) * (mg::kBinT / 32);
   int occ = 1;
   MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mg::k_bin_reduce, mg::kBinT, red_smem));
@@ -537,19 +547,27 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
         nunit);
     ctx->end();
     ctx->begin(MAGNUS_K_BIN_EXPAND);
-    mg::k_bin_expand<<<(unsigned)(ctx->sm_count * occ_e), mg::kBinT, 0, s>>>(
+#ifndef MG_EXP_CTAS
+#define MG_EXP_CTAS occ_e
+#endif
+    mg::k_bin_expand<<<(unsigned)(ctx->sm_count * std::min(occ_e, MG_EXP_CTAS)), mg::kBinT, 0, s>>>(
         ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
         nunit, nwin + 3, static_cast<uint16_t*>(bcol), static_cast<double*>(bval));
     ctx->end();
+    // the big-chunk and small-chunk reducers are independent: run them side by side
+    // (profiled together as MAGNUS_K_BIN_REDUCE)
     ctx->begin(MAGNUS_K_BIN_REDUCE);
+    MG_CUDA(cudaEventRecord(ctx->ev_fork, s));
+    MG_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+    mg::k_bin_big<<<(unsigned)(ctx->sm_count * occ_b), 32, big_smem, ctx->aux>>>(
+        ctx->listH, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->hbase, hb[b], bigs, nbig, nwin + 5,
+        static_cast<const uint16_t*>(bcol), static_cast<const double*>(bval), c_rp, c_col, c_val, ctx->err);
+    ++ctx->launches;
+    MG_CUDA(cudaEventRecord(ctx->ev_join, ctx->aux));
     mg::k_bin_reduce<<<(unsigned)(ctx->sm_count * occ), mg::kBinT, red_smem, s>>>(
         ctx->listH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->hbase, hb[b], wins, nwin,
         nwin + 4, static_cast<const uint16_t*>(bcol), static_cast<const double*>(bval), c_rp, c_col, c_val, ctx->err);
-    ctx->end();
-    ctx->begin(MAGNUS_K_BIN_BIG);
-    mg::k_bin_big<<<(unsigned)(ctx->sm_count * occ_b), mg::kBigT, big_smem, s>>>(
-        ctx->listH, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->hbase, hb[b], bigs, nbig, nwin + 5,
-        static_cast<const uint16_t*>(bcol), static_cast<const double*>(bval), c_rp, c_col, c_val, ctx->err);
+    MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_join, 0));
     ctx->end();
     MG_CUDA(cudaGetLastError());
   }

@@ -8,6 +8,10 @@ sys.path.insert(0, ROOT)
 os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 import torch  # noqa: E402
 
+from paper_2501_07056_b200 import _lib  # noqa: E402
+
+if os.environ.get("PHASE_LIB"):   # a variant build (tools/variants.py)
+    _lib.LIB_PATH = os.environ["PHASE_LIB"]
 from paper_2501_07056_b200 import MagnusPlan, detect_device_params, generate  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
