@@ -139,7 +139,12 @@ def algorithmic_bytes(A, B, inter, c_nnz_row, rp_bytes_a, rp_bytes_b):
         b_rp = nkm * 2 * rp_bytes_b
         sym = a_bytes - nkm * 8 + b_rp + im * 4 + rows * 8
         num = a_bytes + b_rp + im * 12 + cm * 12 + rows * 16
-        out[name] = {"rows": rows, "inter": im, "nnz_c": cm, "sym_bytes": sym, "num_bytes": num}
+        # binned heavy path: expand reads A and the B rows, writes the reorder
+        # buffer (u16 column + f64 product); the reducers read the buffer and write C
+        exp_b = a_bytes + b_rp + im * 12 + im * 10
+        red_b = im * 10 + cm * 12 + rows * 16
+        out[name] = {"rows": rows, "inter": im, "nnz_c": cm, "sym_bytes": sym, "num_bytes": num,
+                     "expand_bytes": exp_b, "reduce_bytes": red_b}
     return out
 
 
@@ -288,12 +293,16 @@ def main():
     del C
     peak, peak_kind = hbm_peak()
     kern_bytes = {"num_heavy": ab["heavy"]["num_bytes"], "sym_heavy": ab["heavy"]["sym_bytes"],
+                  "bin_expand": ab["heavy"]["expand_bytes"], "bin_reduce": ab["heavy"]["reduce_bytes"],
                   "num_dense": ab["dense"]["num_bytes"], "sym_dense": ab["dense"]["sym_bytes"],
                   "num_block": ab["block"]["num_bytes"], "sym_block": ab["block"]["sym_bytes"],
                   "num_warp": ab["warp"]["num_bytes"], "sym_warp": ab["warp"]["sym_bytes"]}
     dom = max(prof, key=lambda k: prof[k][0])
-    dom_ms = prof[dom][0] / max(prof[dom][1], 1)
+    nl_dom = max(prof[dom][1], 1)
+    dom_ms = prof[dom][0] / nl_dom
     dom_bytes = kern_bytes.get(dom)
+    if dom_bytes is not None:
+        dom_bytes = dom_bytes // nl_dom   # the class's bytes are split over its launches (row batches)
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_bytes else None
     prof_share = {k: round(v[0], 3) for k, v in prof.items() if v[1]}
 

@@ -157,9 +157,31 @@ __global__ void __launch_bounds__(kWT) k_rows_warp(DevCsr A, DevCsr B, const int
 }
 
 // ================================================================ CTA per row
+// Rows with 256 < products <= 4096: the product is gathered in Gustavson order
+// (one ascending run per B row), then the runs are merged pairwise (merge path,
+// ties from the left run: a stable sort by column that keeps ascending k inside
+// every column), then each column is summed by one thread with the association
+// the reference gives it.
 constexpr int kBT = 256;
 constexpr int kBSlots = 4096;
-constexpr int kBSmem = kBSlots * 16 + (kBT + 4 + kBT + 64) * 4;
+constexpr size_t kBSmem = (size_t)kBSlots * 4 * 2      // keys (ping-pong)
+                          + (size_t)kBSlots * 2 * 2    // positions (ping-pong)
+                          + (size_t)kBSlots * 8        // values (stream order)
+                          + (size_t)(kBSlots + 8) * 2  // run boundaries
+                          + (size_t)(kBSlots + 8) * 2  // column starts
+                          + (size_t)(kBT + 8) * 4 * 2  // k offsets / starts
+                          + 64 * 4;
+
+// merge path: number of elements taken from L when d outputs of merge(L, R) are done
+// (stable: on equal keys L goes first)
+__device__ __forceinline__ int merge_split(const uint32_t* L, int nl, const uint32_t* R, int nr, int d) {
+  int lo = max(0, d - nr), hi = min(d, nl);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (L[mid] <= R[d - 1 - mid]) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
 
 template <bool Numeric>
 __global__ void __launch_bounds__(kBT) k_rows_block(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows,
@@ -167,20 +189,27 @@ __global__ void __launch_bounds__(kBT) k_rows_block(DevCsr A, DevCsr B, const in
                                                     const int64_t* __restrict__ c_rp, uint32_t* __restrict__ c_col,
                                                     double* __restrict__ c_val, unsigned long long* __restrict__ err) {
   extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem);
-  double* vals = reinterpret_cast<double*>(smem + kBSlots * 8);
-  uint32_t* koff = reinterpret_cast<uint32_t*>(smem + kBSlots * 16);  // kBT + 1 entries
-  uint32_t* kb0 = koff + (kBT + 4);
-  uint32_t* scratch = kb0 + kBT;
+  unsigned char* sp = smem;
+  uint32_t* keyA = reinterpret_cast<uint32_t*>(sp); sp += kBSlots * 4;
+  uint32_t* keyB = reinterpret_cast<uint32_t*>(sp); sp += kBSlots * 4;
+  double* vals = reinterpret_cast<double*>(sp); sp += kBSlots * 8;
+  uint16_t* posA = reinterpret_cast<uint16_t*>(sp); sp += kBSlots * 2;
+  uint16_t* posB = reinterpret_cast<uint16_t*>(sp); sp += kBSlots * 2;
+  uint16_t* runs = reinterpret_cast<uint16_t*>(sp); sp += (kBSlots + 8) * 2;
+  uint16_t* cst = reinterpret_cast<uint16_t*>(sp); sp += (kBSlots + 8) * 2;
+  uint32_t* koff = reinterpret_cast<uint32_t*>(sp); sp += (kBT + 8) * 4;
+  uint32_t* kb0 = reinterpret_cast<uint32_t*>(sp); sp += (kBT + 8) * 4;
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(sp);
   __shared__ double s_av[kBT];
-  __shared__ uint32_t s_heads[kBT + 1];
-  const int tid = threadIdx.x;
+  __shared__ int s_nr;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 
   for (int64_t w = blockIdx.x; w < nrows; w += gridDim.x) {
     const int64_t i = rows[w];
     const int64_t a0 = A.rp(i), a1 = A.rp(i + 1);
     uint32_t base = 0;
-    // gather in chunks of kBT k's: lengths -> scan -> cooperative copy
+    if (tid == 0) s_nr = 0;
+    // ---- gather in chunks of kBT k's: lengths -> scan -> cooperative copy; runs = non-empty segments
     for (int64_t t0 = a0; t0 < a1; t0 += kBT) {
       const int64_t t = t0 + tid;
       uint32_t len = 0;
@@ -193,69 +222,154 @@ __global__ void __launch_bounds__(kBT) k_rows_block(DevCsr A, DevCsr B, const in
       }
       koff[tid] = len;
       __syncthreads();
-      const uint32_t tot = block_excl_scan<kBT>(koff, kBT, scratch);
+      const int nr0 = s_nr;
+      const uint32_t ne = __ballot_sync(0xffffffffu, len > 0);
+      if (lane == 0) scratch[wid] = __popc(ne);
+      const uint32_t tot = block_excl_scan<kBT>(koff, kBT, scratch + 8);
       if (tid == 0) koff[kBT] = tot;
+      // run starts of the non-empty segments (in k order)
+      uint32_t wb = 0;
+      for (int q = 0; q < wid; ++q) wb += scratch[q];
+      if (len > 0) runs[nr0 + wb + __popc(ne & ((1u << lane) - 1u))] = (uint16_t)(base + koff[tid]);
       __syncthreads();
-      // element q of this chunk -> segment via binary search over koff
+      if (tid == 0) {
+        uint32_t all = 0;
+        for (int q = 0; q < kBT / 32; ++q) all += scratch[q];
+        s_nr = nr0 + (int)all;
+      }
       for (uint32_t q = tid; q < tot; q += kBT) {
-        int lo = 0, hi = kBT;  // find last seg with koff[seg] <= q
+        int lo = 0, hi = kBT;  // last segment with koff[seg] <= q
         while (hi - lo > 1) {
-          int mid = (lo + hi) >> 1;
+          const int mid = (lo + hi) >> 1;
           if (koff[mid] <= q) lo = mid; else hi = mid;
         }
-        const uint32_t j = q - koff[lo];
-        const uint32_t src = kb0[lo] + j;
+        const uint32_t src = kb0[lo] + (q - koff[lo]);
         const uint32_t p = base + q;
-        const uint32_t c = __ldg(B.col + src);
-        keys[p] = ((unsigned long long)c << 12) | p;
+        keyA[p] = __ldg(B.col + src);
+        posA[p] = (uint16_t)p;
         if (Numeric) vals[p] = __dmul_rn(s_av[lo], __ldg(B.val + src));
       }
       base += tot;
       __syncthreads();
     }
     const int n = (int)base;
-    const int np2 = pow2_at_least(n, 64);
-    for (int p = n + tid; p < np2; p += kBT) keys[p] = ~0ull;
+    int nr = s_nr;
+    if (tid == 0) runs[nr] = (uint16_t)n;
     __syncthreads();
-    bitonic<kBT, false>(keys, np2, tid);
-    // heads: each thread owns a contiguous range of sorted positions
+    // ---- pairwise merge rounds
+    uint32_t* kin = keyA;
+    uint32_t* kout = keyB;
+    uint16_t* pin = posA;
+    uint16_t* pout = posB;
     const int per = (n + kBT - 1) / kBT;
-    const int pb = tid * per, pe = min(n, pb + per);
-    uint32_t nh = 0;
-    for (int p = pb; p < pe; ++p)
-      if (p == 0 || (keys[p - 1] >> 12) != (keys[p] >> 12)) ++nh;
-    s_heads[tid] = nh;
+    while (nr > 1) {
+      const int npair = (nr + 1) >> 1;
+      int o = tid * per;
+      const int oend = min(n, o + per);
+      while (o < oend) {
+        // pair j containing output o: last j with runs[2j] <= o
+        int lo = 0, hi = npair;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if ((int)runs[2 * mid] <= o) lo = mid; else hi = mid;
+        }
+        const int ls = runs[2 * lo], ms = runs[min(2 * lo + 1, nr)], re = runs[min(2 * lo + 2, nr)];
+        const int nl = ms - ls, nrr = re - ms;
+        const int d = o - ls;
+        int li = merge_split(kin + ls, nl, kin + ms, nrr, d);
+        int ri = d - li;
+        const int stop = min(oend, re);
+        for (; o < stop; ++o) {
+          bool takeL;
+          if (li >= nl) takeL = false;
+          else if (ri >= nrr) takeL = true;
+          else takeL = kin[ls + li] <= kin[ms + ri];
+          const int src = takeL ? ls + li : ms + ri;
+          kout[o] = kin[src];
+          pout[o] = pin[src];
+          if (takeL) ++li; else ++ri;
+        }
+      }
+      __syncthreads();
+      // run boundaries of the merged runs
+      constexpr int kNb = kBSlots / kBT + 1;
+      uint16_t nb[kNb];
+      const int nnr = npair;
+#pragma unroll
+      for (int q = 0; q < kNb; ++q) {
+        const int j = tid + q * kBT;
+        if (j <= nnr) nb[q] = j < nnr ? runs[2 * j] : (uint16_t)n;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kNb; ++q) {
+        const int j = tid + q * kBT;
+        if (j <= nnr) runs[j] = nb[q];
+      }
+      __syncthreads();
+      nr = nnr;
+      uint32_t* tk = kin; kin = kout; kout = tk;
+      uint16_t* tp = pin; pin = pout; pout = tp;
+    }
+    // ---- column heads: warp w scans a contiguous slice of the sorted keys with ballots
+    const int sl = ((n + kBT / 32 - 1) / (kBT / 32) + 31) & ~31;
+    const int s0 = min(n, wid * sl), s1 = min(n, s0 + sl);
+    uint32_t wcount = 0;
+    for (int p0 = s0; p0 < s1; p0 += 32) {
+      const int p = p0 + lane;
+      const bool head = p < s1 && (p == 0 || kin[p - 1] != kin[p]);
+      wcount += __popc(__ballot_sync(0xffffffffu, head));
+    }
+    if (lane == 0) scratch[wid] = wcount;
     __syncthreads();
-    const uint32_t total = block_excl_scan<kBT>(s_heads, kBT, scratch);
+    uint32_t rb = 0, total = 0;
+    for (int q = 0; q < kBT / 32; ++q) {
+      const uint32_t v = scratch[q];
+      if (q < wid) rb += v;
+      total += v;
+    }
+    for (int p0 = s0; p0 < s1; p0 += 32) {
+      const int p = p0 + lane;
+      const bool head = p < s1 && (p == 0 || kin[p - 1] != kin[p]);
+      const uint32_t m = __ballot_sync(0xffffffffu, head);
+      if (head) cst[rb + __popc(m & ((1u << lane) - 1u))] = (uint16_t)p;
+      rb += __popc(m);
+    }
+    if (tid == 0) cst[total] = (uint16_t)n;
+    __syncthreads();
     if (Numeric) {
       const int ci = (int)cat[i];
       const int64_t out0 = c_rp[i];
       const int64_t out_n = c_rp[i + 1] - out0;
-      uint32_t r = s_heads[tid];
-      for (int p = pb; p < pe; ++p) {
-        const unsigned long long c = keys[p] >> 12;
-        if (!(p == 0 || (keys[p - 1] >> 12) != c)) continue;
-        int e = p + 1;
-        while (e < n && (keys[e] >> 12) == c) ++e;
+      for (uint32_t r = tid; r < total; r += kBT) {
+        const int p = cst[r], e = cst[r + 1];
+        const uint32_t c = kin[p];
         auto chunk_count = [&]() -> int64_t {
-          const unsigned long long f = c >> sem.shift_num;
-          const unsigned long long lo = (f << sem.shift_num) << 12, hi = ((f + 1) << sem.shift_num) << 12;
-          return lb_smem(keys, n, hi) - lb_smem(keys, n, lo);
+          const uint64_t f = (uint64_t)c >> sem.shift_num;
+          const uint64_t lo = f << sem.shift_num, hi = (f + 1) << sem.shift_num;
+          auto lb = [&](uint64_t key) {
+            int a = 0, b = n;
+            while (a < b) {
+              const int mid = (a + b) >> 1;
+              if ((uint64_t)kin[mid] < key) a = mid + 1; else b = mid;
+            }
+            return a;
+          };
+          return lb(hi) - lb(lo);
         };
-        double s;
+        double sum;
         if (seq_mode(ci, sem, chunk_count)) {
-          s = 0.0;
-          for (int q = p; q < e; ++q) s = __dadd_rn(s, vals[keys[q] & 0xFFF]);
+          sum = 0.0;
+          for (int q = p; q < e; ++q) sum = __dadd_rn(sum, vals[pin[q]]);
         } else {
-          auto x = [&](int64_t q) { return vals[keys[q] & 0xFFF]; };
-          s = vals[keys[p] & 0xFFF];
-          if (e - p > 1) s = __dadd_rn(s, pairwise(x, p + 1, e - p - 1));
+          auto x = [&](int64_t q) { return vals[pin[q]]; };
+          sum = vals[pin[p]];
+          if (e - p > 1) sum = __dadd_rn(sum, pairwise(x, p + 1, e - p - 1));
         }
-        if (r < out_n) {
-          c_col[out0 + r] = (uint32_t)c;
-          c_val[out0 + r] = s;
+        if ((int64_t)r < out_n) {
+          c_col[out0 + r] = c;
+          c_val[out0 + r] = sum;
         }
-        ++r;
       }
       if (tid == 0 && total != out_n) atomicOr(err, 1ull);
     } else if (tid == 0) {
