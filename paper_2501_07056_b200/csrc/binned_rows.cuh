@@ -43,7 +43,7 @@ constexpr int kBinWinT = kBinE / 2;   // window packing quantum
 constexpr int kBinMaxShift = 14;      // chunk width <= 16384 columns (u16 chunk-local columns)
 constexpr int kSubShift = 14;         // table granularity (sub-bin == chunk while shift_num <= 14)
 constexpr int kBinCur = 1024;         // expand: chunk cursors per warp (shared memory)
-constexpr int64_t kBinUnitMax = 1 << 18;   // expand: elements per unit (rows above are split by chunk ranges)
+constexpr int64_t kBinUnitMax = 1 << 17;   // expand: elements per unit (rows above are split by chunk ranges)
 #ifndef MG_EXP_U
 #define MG_EXP_U 8
 #endif
@@ -52,6 +52,8 @@ constexpr int64_t kBinUnitMax = 1 << 18;   // expand: elements per unit (rows ab
 #endif
 constexpr int kBinU = MG_EXP_U;       // waves of loads in flight per lane
 constexpr uint32_t kBigSplit = 1u << 17;   // big chunks above this many elements are split by columns
+constexpr uint32_t kBigFront = 1u << 14;   // big chunks scheduled first
+constexpr uint32_t kUnitFront = 1u << 15;  // expand units scheduled first
 constexpr int kBigMaxParts = 32;
 
 __host__ __device__ inline int bin_shift_of(int shift_num) { return shift_num < kSubShift ? shift_num : kSubShift; }
@@ -64,8 +66,8 @@ struct BinItem {   // table entries (sub-bins) [ja, jb) of heavy row h
 __host__ __device__ inline size_t bin_reduce_warp_smem(int shift) {
   const size_t words = shift >= 5 ? (size_t(1) << (shift - 5)) : 1;
   const size_t w4 = (words * 4 + 15) & ~size_t(15), w2 = (words * 2 + 15) & ~size_t(15);
-  return w4 + w2 + (size_t)kBinE * 2 /*u16 counts*/ + (size_t)kBinE * 8 /*values | dense window*/ +
-         (size_t)kBinE * 2 /*columns*/;
+  return w4 + w2 + (size_t)kBinE * 2 /*u16 counts*/ + (size_t)kBinE * 8 /*values*/ + (size_t)kBinE * 2 /*columns*/ +
+         (size_t)kBinE * 2 /*rank -> column*/;
 }
 
 // per heavy row: table entries (sub-bins in [mn >> gs, mx >> gs] plus one total) and its stream size
@@ -85,14 +87,23 @@ __device__ __forceinline__ uint32_t lanemask_le() {
   return l == 31 ? 0xffffffffu : ((2u << l) - 1u);
 }
 
-// warp-aggregated append of the items whose flag is set
-__device__ __forceinline__ void emit_items(bool flag, BinItem it, BinItem* out, unsigned long long* count) {
+// warp-aggregated append of the items whose flag is set (rev: placed from the end of a
+// list of `cap` slots downwards)
+__device__ __forceinline__ void emit_items(bool flag, BinItem it, BinItem* out, unsigned long long* count,
+                                           int64_t rev_cap = -1) {
   const uint32_t m = __ballot_sync(0xffffffffu, flag);
   if (!m) return;
   unsigned long long base = 0;
   if ((threadIdx.x & 31) == 0) base = atomicAdd(count, (unsigned long long)__popc(m));
   base = __shfl_sync(0xffffffffu, base, 0);
-  if (flag) out[base + __popc(m & lanemask_lt())] = it;
+  const int64_t pos = (int64_t)base + __popc(m & lanemask_lt());
+  if (flag) out[rev_cap < 0 ? pos : rev_cap - 1 - pos] = it;
+}
+
+// Lists with large items first: items [0, n_front) are the large ones, the others sit at
+// [cap - n_back, cap) -- scheduling ticket t maps to the t-th item of that order.
+__device__ __forceinline__ int64_t list_slot(uint64_t t, uint64_t n_front, int64_t cap) {
+  return t < n_front ? (int64_t)t : cap - 1 - (int64_t)(t - n_front);
 }
 
 // Geometry of one heavy row in table-entry space.
@@ -122,8 +133,10 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
                            const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff,
                            const uint32_t* __restrict__ ce, BinItem* __restrict__ wins, unsigned long long* __restrict__ nwin,
                            BinItem* __restrict__ bigs, unsigned long long* __restrict__ nbig, BinItem* __restrict__ units,
-                           unsigned long long* __restrict__ nunit) {
+                           unsigned long long* __restrict__ nunit, int64_t cap_units, int64_t cap_bigs) {
   const int lane = threadIdx.x & 31;
+  unsigned long long* nunit_back = nwin + 6;
+  unsigned long long* nbig_back = nwin + 7;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t h = h0 + warp; h < h1; h += nwarps) {
@@ -155,8 +168,10 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
       // streams the whole slice but applies only its own columns)
       if (big) {
         const int parts = (int)min((uint32_t)kBigMaxParts, (n + kBigSplit - 1) / kBigSplit);
-        const unsigned long long b0i = atomicAdd(nbig, (unsigned long long)parts);
-        for (int pp = 0; pp < parts; ++pp) bigs[b0i + pp] = BinItem{(int32_t)h, js, je, (parts << 16) | pp};
+        const bool large = n >= kBigFront;
+        const unsigned long long b0i = atomicAdd(large ? nbig : nbig_back, (unsigned long long)parts);
+        for (int pp = 0; pp < parts; ++pp)
+          bigs[large ? (int64_t)(b0i + pp) : cap_bigs - 1 - (int64_t)(b0i + pp)] = BinItem{(int32_t)h, js, je, (parts << 16) | pp};
       }
       // ---- expand units: chunk ranges (whole chunks, so small-chunk slices stay in one unit)
       const bool ucut = valid && (cj == rb.nchunk - 1 ||
@@ -167,7 +182,10 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
         const uint32_t prev = um & lanemask_lt();
         const int us = prev ? q0 + 31 - __clz(prev) + 1 : ustart;
         const int ujs = rb.js(us);
-        emit_items(ucut && pi > __ldg(e + ujs), BinItem{(int32_t)h, ujs, je, split ? 0 : 1}, units, nunit);
+        const uint32_t un = pi - __ldg(e + ujs);
+        const bool uemit = ucut && un > 0;
+        emit_items(uemit && un >= kUnitFront, BinItem{(int32_t)h, ujs, je, split ? 0 : 1}, units, nunit);
+        emit_items(uemit && un < kUnitFront, BinItem{(int32_t)h, ujs, je, split ? 0 : 1}, units, nunit_back, cap_units);
         if (um) ustart = q0 + 31 - __clz(um) + 1;
       }
     }
@@ -179,7 +197,7 @@ __global__ void __launch_bounds__(kBinT, MG_EXP_MINB)
 k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t* __restrict__ mn,
              const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce,
              const int64_t* __restrict__ hbase, int64_t batch_base, const BinItem* __restrict__ units,
-             const unsigned long long* __restrict__ nunit, unsigned long long* __restrict__ ticket,
+             const unsigned long long* __restrict__ nunit, unsigned long long* __restrict__ ticket, int64_t cap_units,
              uint16_t* __restrict__ bcol, double* __restrict__ bval) {
   __shared__ uint32_t s_cur[kBinT / 32][kBinCur];
   __shared__ uint32_t s_big[kBinT / 32][kBinCur / 32];   // big-chunk flags of the unit's chunks
@@ -187,14 +205,14 @@ k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t
   uint32_t* cur = s_cur[threadIdx.x >> 5];
   uint32_t* bigm = s_big[threadIdx.x >> 5];
   const int gs = bin_shift_of(shift);
-  const int64_t nu = (int64_t)*nunit;
+  const uint64_t nu_front = nunit[0], nu = nu_front + nunit[5];   // nunit[5] = back counter (cnts[6])
   const uint32_t cmask = (1u << shift) - 1u;
   while (true) {
     unsigned long long u = 0;
     if (lane == 0) u = atomicAdd(ticket, 1ull);
     u = __shfl_sync(0xffffffffu, u, 0);
-    if ((int64_t)u >= nu) break;
-    const BinItem it = units[u];
+    if (u >= nu) break;
+    const BinItem it = units[list_slot(u, nu_front, cap_units)];
     const int64_t i = rows[it.h];
     const int64_t a0 = A.rp(i), a1 = A.rp(i + 1);
     const RowBins rb = row_bins(mn[i], mx[i], shift);
@@ -256,18 +274,23 @@ k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t
           // ---- one long B row
           const uint32_t bb0 = __shfl_sync(0xffffffffu, p0, ts), bb1 = __shfl_sync(0xffffffffu, p1, ts);
           const double a = __shfl_sync(0xffffffffu, av, ts);
+          // software pipeline: the loads of the next 32 * kBinU products are in flight while
+          // the current ones are placed
+          uint32_t c[kBinU], cn[kBinU];
+          double v[kBinU], vn[kBinU];
+#pragma unroll
+          for (int w = 0; w < kBinU; ++w) {
+            const uint32_t pp = bb0 + w * 32 + lane;
+            c[w] = pp < bb1 ? __ldg(B.col + pp) : 0xffffffffu;
+            v[w] = pp < bb1 ? __ldg(B.val + pp) : 0.0;
+          }
           for (uint32_t q0 = bb0; q0 < bb1; q0 += 32 * kBinU) {
-            uint32_t c[kBinU];
-            double v[kBinU];
+            const uint32_t q1 = q0 + 32 * kBinU;
 #pragma unroll
             for (int w = 0; w < kBinU; ++w) {
-              const uint32_t pp = q0 + w * 32 + lane;
-              c[w] = 0xffffffffu;
-              v[w] = 0.0;
-              if (pp < bb1) {
-                c[w] = __ldg(B.col + pp);
-                v[w] = __dmul_rn(a, __ldg(B.val + pp));
-              }
+              const uint32_t pp = q1 + w * 32 + lane;
+              cn[w] = pp < bb1 ? __ldg(B.col + pp) : 0xffffffffu;
+              vn[w] = pp < bb1 ? __ldg(B.val + pp) : 0.0;
             }
 #pragma unroll
             for (int w = 0; w < kBinU; ++w) {
@@ -283,12 +306,21 @@ k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t
                 if (valid) slot = cur[fl] + rank;
                 __syncwarp();
                 if (valid && last) cur[fl] = slot + 1;
+#ifdef MG_EXP_NOSTORE
+                if (valid && slot == 0xfffffff0u) {
+#else
                 if (valid) {
+#endif
                   rc[slot] = (uint16_t)(c[w] & cmask);
-                  rv[slot] = v[w];
+                  rv[slot] = __dmul_rn(a, v[w]);
                 }
                 __syncwarp();
               }
+            }
+#pragma unroll
+            for (int w = 0; w < kBinU; ++w) {
+              c[w] = cn[w];
+              v[w] = vn[w];
             }
           }
           ++ts;
@@ -395,6 +427,7 @@ struct ReduceSmem {
   uint32_t* cnt;
   double* sval;
   uint16_t* stc;
+  uint16_t* inv;   // rank -> column
 };
 
 // Small chunk (n <= kBinE elements): stable counting sort of the slice by column rank
@@ -426,7 +459,9 @@ __device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* __restrict__ s
   __syncwarp();
   if (prefix_words(S.bm, S.pref, wlo, whi) != m) return false;
   for (uint32_t q = lane; q < n; q += 32) {
-    const uint32_t r = rank_of(S.bm, S.pref, S.stc[q]);
+    const uint32_t c = S.stc[q];
+    const uint32_t r = rank_of(S.bm, S.pref, c);
+    S.inv[r] = (uint16_t)c;
     S.stc[q] = (uint16_t)r;   // the slice's columns become ranks
     atomicAdd(&S.cnt[r >> 1], 1u << ((r & 1u) * 16));
   }
@@ -474,17 +509,8 @@ __device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* __restrict__ s
   __syncwarp();
   for (uint32_t r = lane; r < m; r += 32) {
     const uint32_t s0 = r ? u16_get(S.cnt, r - 1) : 0u, e0 = u16_get(S.cnt, r);
+    c_col[out + r] = colbase + S.inv[r];
     c_val[out + r] = seq ? sum_seq_s(S.sval, s0, e0) : sum_pairwise_s(S.sval, s0, e0);
-  }
-  for (int wd = wlo + lane; wd < whi; wd += 32) {
-    uint32_t bits = S.bm[wd];
-    uint32_t r = S.pref[wd];
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1u;
-      c_col[out + r] = colbase + (uint32_t)(wd * 32 + b);
-      ++r;
-    }
   }
   __syncwarp();
   return true;
@@ -510,6 +536,7 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
   S.cnt = reinterpret_cast<uint32_t*>(base + w4 + w2);
   S.sval = reinterpret_cast<double*>(base + w4 + w2 + (size_t)kBinE * 2);
   S.stc = reinterpret_cast<uint16_t*>(base + w4 + w2 + (size_t)kBinE * 10);
+  S.inv = reinterpret_cast<uint16_t*>(base + w4 + w2 + (size_t)kBinE * 12);
   const int64_t nw = (int64_t)*nwin;
   const uint32_t cwmask = ~((1u << shift) - 1u);
   while (true) {
@@ -549,41 +576,105 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
 // shared-memory accumulator indexed by rank, kBigD ranks per pass (as the
 // reference's dense accumulator, accumulators.py:68-97).  Inside one wave the
 // lanes of a repeated column are added by the lowest of them, in lane order.
-// Loads run kBigU waves ahead.  Chunks above kBigSplit elements are split into
-// column parts handled by different warps.
-constexpr int kBigU = 8;
+// The slice streams through a ring of kBigNS shared-memory stages filled by
+// asynchronous bulk copies (cp.async.bulk, completion on an mbarrier), so many
+// bytes per warp are in flight without registers.  Chunks above kBigSplit
+// elements are split into column parts handled by different warps.
 #ifndef MG_BIG_D
 #define MG_BIG_D 2048
 #endif
-constexpr int kBigD = MG_BIG_D;   // ranks accumulated per pass (16 KB)
+constexpr int kBigD = MG_BIG_D;            // ranks accumulated per pass
+#ifndef MG_BIG_RS
+#define MG_BIG_RS 3
+#endif
+constexpr int kBigRunSer = MG_BIG_RS;      // waves with fewer run breaks are applied run by run
+constexpr int kBigNS = 4;                  // ring stages per warp
+constexpr int kBigSE = 256;                // elements per stage
+constexpr int kBigSC = kBigSE * 2 + 16;    // stage bytes: columns (+ alignment slack)
+constexpr int kBigSV = kBigSE * 8 + 16;    // stage bytes: values (+ alignment slack)
+#ifdef MG_BIG_STATS
+__device__ unsigned long long g_big_stats[8];
+#endif
 
 __host__ __device__ inline size_t bin_big_smem(int shift) {
   const size_t width = size_t(1) << shift, words = (width + 31) / 32;
-  return (size_t)kBigD * 8 + ((words * 4 + 15) & ~size_t(15)) + ((words * 2 + 15) & ~size_t(15));
+  return (size_t)kBigD * 8 + (size_t)kBigD * 2 + ((words * 4 + 15) & ~size_t(15)) + ((words * 2 + 15) & ~size_t(15)) +
+         (size_t)kBigNS * (kBigSC + kBigSV) + kBigNS * 8;
 }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// one thread: expect `bytes` on bar, then issue the two bulk copies that complete them
+__device__ __forceinline__ void bulk_load2(uint64_t* bar, void* d0, const void* s0, uint32_t n0, void* d1, const void* s1,
+                                           uint32_t n1) {
+  asm volatile(
+      "{\n .reg .b64 st;\n"
+      " mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(n0 + n1)
+      : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(d0)),
+               "l"(s0), "r"(n0), "r"(smem_u32(bar))
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(d1)),
+               "l"(s1), "r"(n1), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+struct BigStage {
+  const uint16_t* c;   // columns of stage elements (offset applied)
+  const double* v;
+};
 
 __global__ void __launch_bounds__(32)
 k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, const int64_t* __restrict__ mx, Sem sem,
           const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce, const uint32_t* __restrict__ cd,
           const int64_t* __restrict__ hbase, int64_t batch_base, const BinItem* __restrict__ bigs,
-          const unsigned long long* __restrict__ nbig, unsigned long long* __restrict__ ticket,
+          const unsigned long long* __restrict__ nbig, unsigned long long* __restrict__ ticket, int64_t cap_bigs,
+          const uint32_t* __restrict__ cbm_pool, const uint32_t* __restrict__ cbm_slot,
           const uint16_t* __restrict__ bcol, const double* __restrict__ bval, const int64_t* __restrict__ c_rp,
           uint32_t* __restrict__ c_col, double* __restrict__ c_val, unsigned long long* __restrict__ err) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int shift = sem.shift_num;
   const uint32_t width = 1u << shift;
   const int nwords = (int)((width + 31) / 32);
-  double* acc = reinterpret_cast<double*>(smem);
-  uint32_t* bm = reinterpret_cast<uint32_t*>(smem + (size_t)kBigD * 8);
-  uint16_t* pref = reinterpret_cast<uint16_t*>(smem + (size_t)kBigD * 8 + (((size_t)nwords * 4 + 15) & ~size_t(15)));
+  unsigned char* sp = smem;
+  double* acc = reinterpret_cast<double*>(sp); sp += (size_t)kBigD * 8;
+  unsigned char* stv0 = sp; sp += (size_t)kBigNS * kBigSV;   // 16-byte aligned (kBigD * 8 is)
+  unsigned char* stc0 = sp; sp += (size_t)kBigNS * kBigSC;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sp); sp += kBigNS * 8;
+  uint16_t* inv = reinterpret_cast<uint16_t*>(sp); sp += (size_t)kBigD * 2;   // rank - rlo -> column
+  uint32_t* bm = reinterpret_cast<uint32_t*>(sp); sp += ((size_t)nwords * 4 + 15) & ~size_t(15);
+  uint16_t* pref = reinterpret_cast<uint16_t*>(sp);
   const int lane = threadIdx.x & 31;
-  const int64_t nbg = (int64_t)*nbig;
+  if (lane == 0) {
+    for (int q = 0; q < kBigNS; ++q) mbar_init(bars + q);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t uses = 0;   // stage fills issued so far (ring position and parity)
+  const uint64_t nb_front = nbig[0], nbg = nb_front + nbig[5];   // nbig[5] = back counter (cnts[7])
   while (true) {
     unsigned long long bi = 0;
     if (lane == 0) bi = atomicAdd(ticket, 1ull);
     bi = __shfl_sync(0xffffffffu, bi, 0);
-    if ((int64_t)bi >= nbg) break;
-    const BinItem it = bigs[bi];
+    if (bi >= nbg) break;
+    const BinItem it = bigs[list_slot(bi, nb_front, cap_bigs)];
     const int64_t i = rows[it.h];
     const RowBins rb = row_bins(mn[i], mx[i], shift);
     const uint32_t* e = ce + choff[it.h];
@@ -597,18 +688,26 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
     const uint32_t colbase = (uint32_t)(((rb.b0 + it.ja) >> rb.cs) << shift);
     const uint32_t parts = (uint32_t)it.kind >> 16, part = (uint32_t)it.kind & 0xffffu;
     const uint32_t plo = (uint32_t)(((uint64_t)width * part) / parts), phi = (uint32_t)(((uint64_t)width * (part + 1)) / parts);
-    // ---- columns of the chunk -> ranks
-    for (int wd = lane; wd < nwords; wd += 32) bm[wd] = 0u;
+#ifdef MG_BIG_STATS
+    long long t_a = clock64();
+#endif
+    // ---- columns of the chunk -> ranks (bitmap kept by the symbolic pass, else marked here)
+    const uint32_t bslot = cbm_slot != nullptr ? __ldg(cbm_slot + choff[it.h] + it.ja) : 0xffffffffu;
+    if (bslot != 0xffffffffu) {
+      for (int wd = lane; wd < nwords; wd += 32) bm[wd] = __ldg(cbm_pool + (size_t)bslot * nwords + wd);
+    } else {
+      for (int wd = lane; wd < nwords; wd += 32) bm[wd] = 0u;
+    }
     __syncwarp();
-    for (uint32_t q0 = 0; q0 < n; q0 += 32 * kBigU) {
-      uint32_t cc[kBigU];
+    for (uint32_t q0 = 0; bslot == 0xffffffffu && q0 < n; q0 += 32 * 8) {
+      uint32_t cc[8];
 #pragma unroll
-      for (int w = 0; w < kBigU; ++w) {
+      for (int w = 0; w < 8; ++w) {
         const uint32_t q = q0 + w * 32 + lane;
         cc[w] = q < n ? (uint32_t)__ldg(sc + q) : 0xffffffffu;
       }
 #pragma unroll
-      for (int w = 0; w < kBigU; ++w)
+      for (int w = 0; w < 8; ++w)
         if (cc[w] != 0xffffffffu) atomicOr(&bm[cc[w] >> 5], 1u << (cc[w] & 31));
     }
     __syncwarp();
@@ -616,85 +715,124 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
       if (lane == 0) atomicOr(err, 4ull);
       continue;
     }
+#ifdef MG_BIG_STATS
+    long long t_b = clock64();
+    if (lane == 0) atomicAdd(&g_big_stats[4], (unsigned long long)(t_b - t_a));
+#endif
     const uint32_t rlo0 = plo < width ? rank_of(bm, pref, plo) : m;
     const uint32_t rhi0 = phi < width ? rank_of(bm, pref, phi) : m;
-    // ---- columns of this part, ascending
-    for (int wd = (int)(plo >> 5) + lane; wd < (int)((phi + 31) >> 5); wd += 32) {
-      uint32_t bits = bm[wd];
-      const uint32_t lo_b = wd * 32u < plo ? plo - wd * 32u : 0u, hi_b = phi - wd * 32u;
-      if (lo_b) bits &= ~((1u << lo_b) - 1u);
-      if (hi_b < 32u) bits &= (1u << hi_b) - 1u;
-      uint32_t r = pref[wd] + __popc(bm[wd] & (lo_b ? (1u << lo_b) - 1u : 0u));
-      while (bits) {
-        const int b = __ffs(bits) - 1;
-        bits &= bits - 1u;
-        c_col[out + r] = colbase + (uint32_t)(wd * 32 + b);
-        ++r;
+    const uint32_t nst = (n + kBigSE - 1) / kBigSE;   // stages of one pass over the slice
+    // stage j of the slice -> ring slot; copies of 16-byte aligned supersets
+    auto issue = [&](uint32_t j) {
+      const uint32_t slot = uses % kBigNS;
+      ++uses;
+      if (lane == 0) {
+        const uint32_t q0 = j * kBigSE, cnt = min((uint32_t)kBigSE, n - q0);
+        const uintptr_t ca = reinterpret_cast<uintptr_t>(sc + q0), va = reinterpret_cast<uintptr_t>(sv + q0);
+        const uintptr_t ca0 = ca & ~uintptr_t(15), va0 = va & ~uintptr_t(15);
+        const uint32_t cb = (uint32_t)(((ca + cnt * 2 - ca0) + 15) & ~uintptr_t(15));
+        const uint32_t vb = (uint32_t)(((va + cnt * 8 - va0) + 15) & ~uintptr_t(15));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        bulk_load2(bars + slot, stc0 + (size_t)slot * kBigSC, reinterpret_cast<const void*>(ca0), cb,
+                   stv0 + (size_t)slot * kBigSV, reinterpret_cast<const void*>(va0), vb);
       }
-    }
-    // ---- sums, kBigD ranks per pass; loads of the next kBigU waves in flight
+    };
+    // ---- sums, kBigD ranks per pass
     for (uint32_t rlo = rlo0; rlo < rhi0; rlo += kBigD) {
       const uint32_t rhi = min(rhi0, rlo + kBigD);
       for (uint32_t r = lane; r < rhi - rlo; r += 32) acc[r] = 0.0;
+      const uint32_t u0 = uses;   // ring use index of stage 0 of this pass
+      for (uint32_t j = 0; j < min(nst, (uint32_t)kBigNS); ++j) issue(j);
       __syncwarp();
-      uint32_t cc[kBigU], cn[kBigU];
-      double vv[kBigU], vn[kBigU];
+      for (uint32_t j = 0; j < nst; ++j) {
+        const uint32_t use = u0 + j, slot = use % kBigNS;
+        mbar_wait(bars + slot, (use / kBigNS) & 1u);
+        const uint32_t q0 = j * kBigSE, cnt = min((uint32_t)kBigSE, n - q0);
+        const uint16_t* cs =
+            reinterpret_cast<const uint16_t*>(stc0 + (size_t)slot * kBigSC) + ((reinterpret_cast<uintptr_t>(sc + q0) & 15) >> 1);
+        const double* vs =
+            reinterpret_cast<const double*>(stv0 + (size_t)slot * kBigSV) + ((reinterpret_cast<uintptr_t>(sv + q0) & 15) >> 3);
+        uint32_t rr[kBigSE / 32];
 #pragma unroll
-      for (int w = 0; w < kBigU; ++w) {
-        const uint32_t q = w * 32 + lane;
-        cc[w] = q < n ? (uint32_t)__ldg(sc + q) : 0xffffffffu;
-        vv[w] = q < n ? __ldg(sv + q) : 0.0;
-      }
-      for (uint32_t q0 = 0; q0 < n; q0 += 32 * kBigU) {
-        const uint32_t q1 = q0 + 32 * kBigU;
-#pragma unroll
-        for (int w = 0; w < kBigU; ++w) {
-          const uint32_t q = q1 + w * 32 + lane;
-          cn[w] = q < n ? (uint32_t)__ldg(sc + q) : 0xffffffffu;
-          vn[w] = q < n ? __ldg(sv + q) : 0.0;
+        for (int w = 0; w < kBigSE / 32; ++w) {
+          const uint32_t q = w * 32 + lane;
+#ifdef MG_BIG_X2
+          rr[w] = q < cnt ? (uint32_t)cs[q] % (rhi0 - rlo0 + 1) + rlo0 : 0xffffffffu;
+#else
+          rr[w] = q < cnt ? rank_of(bm, pref, cs[q]) : 0xffffffffu;
+#endif
         }
-        // ranks of all waves first (independent shared-memory loads), then the ordered updates
-        uint32_t rr[kBigU];
 #pragma unroll
-        for (int w = 0; w < kBigU; ++w) rr[w] = cc[w] != 0xffffffffu ? rank_of(bm, pref, cc[w]) : 0xffffffffu;
-#pragma unroll
-        for (int w = 0; w < kBigU; ++w) {
-          if (q0 + w * 32 < n) {
-            const double v = vv[w];
-            const uint32_t r = rr[w];
-            const bool valid = r >= rlo && r < rhi;
-            const uint32_t key = valid ? r - rlo : 0x10000u + lane;
-            const uint32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
-            const uint32_t brk = __ballot_sync(0xffffffffu, valid && lane > 0 && key <= pk);
-            if (!brk) {
-              if (valid) acc[key] = __dadd_rn(acc[key], v);
-            } else {
-              const uint32_t peers = __match_any_sync(0xffffffffu, key);
-              const uint32_t gsz = __popc(peers);
-              const uint32_t maxg = __reduce_max_sync(0xffffffffu, valid ? gsz : 0u);
-              const bool lead = valid && (peers & lanemask_lt()) == 0u;
-              double sacc = lead ? acc[key] : 0.0;
-              uint32_t rem = peers;
-              for (uint32_t k = 0; k < maxg; ++k) {
-                const int src = rem ? __ffs(rem) - 1 : lane;
-                if (rem) rem &= rem - 1u;
-                const double x = __shfl_sync(0xffffffffu, v, src);
-                if (lead && k < gsz) sacc = __dadd_rn(sacc, x);
-              }
-              if (lead) acc[key] = sacc;
-            }
-            __syncwarp();
+        for (int w = 0; w < kBigSE / 32; ++w) {
+          const uint32_t q = w * 32 + lane;
+          const uint32_t r = rr[w];
+          const bool valid = r >= rlo && r < rhi;
+          const double v = valid ? vs[q] : 0.0;
+          const uint32_t key = valid ? r - rlo : 0x10000u + lane;
+#ifndef MG_BIG_X3
+          if (valid) inv[key] = cs[q];   // every contributor of a column writes the same value
+#endif
+          const uint32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
+          const uint32_t brk = __ballot_sync(0xffffffffu, valid && lane > 0 && key <= pk);
+#ifdef MG_BIG_STATS
+          {
+            const uint32_t vb = __ballot_sync(0xffffffffu, valid);
+            if (lane == 0) atomicAdd(&g_big_stats[0], 1ull);
+            if (lane == 0) atomicAdd(&g_big_stats[3], (unsigned long long)__popc(vb));
           }
+#endif
+#ifdef MG_BIG_X1
+          if (true) {
+#else
+          if (!brk) {
+#endif
+            if (valid) acc[key] = __dadd_rn(acc[key], v);
+          } else if (__popc(brk) < kBigRunSer) {
+            // few ascending runs: apply them one after another
+            const int run = __popc(brk & lanemask_le());
+            const int nruns = __popc(brk) + 1;
+            for (int rr2 = 0; rr2 < nruns; ++rr2) {
+              if (valid && run == rr2) acc[key] = __dadd_rn(acc[key], v);
+              __syncwarp();
+            }
+          } else {
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            const uint32_t gsz = __popc(peers);
+            const uint32_t maxg = __reduce_max_sync(0xffffffffu, valid ? gsz : 0u);
+#ifdef MG_BIG_STATS
+            if (lane == 0) atomicAdd(&g_big_stats[1], 1ull);
+            if (lane == 0) atomicAdd(&g_big_stats[2], (unsigned long long)maxg);
+#endif
+            const bool lead = valid && (peers & lanemask_lt()) == 0u;
+            double sacc = lead ? acc[key] : 0.0;
+            uint32_t rem = peers;
+            for (uint32_t k = 0; k < maxg; ++k) {
+              const int src = rem ? __ffs(rem) - 1 : lane;
+              if (rem) rem &= rem - 1u;
+              const double x = __shfl_sync(0xffffffffu, v, src);
+              if (lead && k < gsz) sacc = __dadd_rn(sacc, x);
+            }
+            if (lead) acc[key] = sacc;
+          }
+          __syncwarp();
         }
-#pragma unroll
-        for (int w = 0; w < kBigU; ++w) {
-          cc[w] = cn[w];
-          vv[w] = vn[w];
-        }
+        // the slot is free again: refill it with the stage kBigNS ahead
+        if (j + kBigNS < nst) issue(j + kBigNS);
       }
       __syncwarp();
-      for (uint32_t r = rlo + lane; r < rhi; r += 32) c_val[out + r] = acc[r - rlo];
+#ifdef MG_BIG_STATS
+      long long t_c = clock64();
+      if (lane == 0) atomicAdd(&g_big_stats[5], (unsigned long long)(t_c - t_b));
+#endif
+      for (uint32_t r = rlo + lane; r < rhi; r += 32) {
+        c_col[out + r] = colbase + inv[r - rlo];
+        c_val[out + r] = acc[r - rlo];
+      }
       __syncwarp();
+#ifdef MG_BIG_STATS
+      t_b = clock64();
+      if (lane == 0) atomicAdd(&g_big_stats[6], (unsigned long long)(t_b - t_c));
+#endif
     }
   }
 }

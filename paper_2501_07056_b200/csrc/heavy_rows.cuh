@@ -195,7 +195,8 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
                  const int64_t* __restrict__ mn, const int64_t* __restrict__ mx, Sem sem, int64_t* __restrict__ counts,
                  uint32_t* __restrict__ modebits, uint32_t* __restrict__ gk, int64_t gk_stride,
                  uint32_t* __restrict__ gchunk, unsigned long long* __restrict__ work, int binned, int64_t ncnt,
-                 const int64_t* __restrict__ choff, uint32_t* __restrict__ ce, uint32_t* __restrict__ cd) {
+                 const int64_t* __restrict__ choff, uint32_t* __restrict__ ce, uint32_t* __restrict__ cd,
+                 uint32_t* __restrict__ cbm_pool, uint32_t* __restrict__ cbm_slot, uint64_t cbm_cap) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem);
   uint32_t* ccnt_s = reinterpret_cast<uint32_t*>(smem + HeavySymSmem::kBitmap);
@@ -294,11 +295,27 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
         } else {
           const int nchw = (words + wpc - 1) / wpc;
           for (int cj = wid; cj < nchw; cj += kHT / 32) {
+            // a chunk too big for the sort reducer: its column bitmap is kept for the
+            // dense reducer (k_bin_big), which then needs no marking pass of its own
+            const int64_t f = (lo >> shift) + cj;
+            const bool big = cbm_pool != nullptr && ccnt[f] > (uint32_t)kBinE;
+            uint32_t slot = 0xffffffffu;
+            if (big) {
+              if (lane == 0) slot = (uint32_t)min((unsigned long long)0xffffffffu, atomicAdd(work + 2, 1ull));
+              slot = __shfl_sync(0xffffffffu, slot, 0);
+              if (slot >= cbm_cap) slot = 0xffffffffu;
+              if (lane == 0) cbm_slot[choff[w] + (f - (row_lo >> shift))] = slot;
+            }
+            uint32_t* dst = slot != 0xffffffffu ? cbm_pool + (size_t)slot * wpc : nullptr;
             uint32_t cp = 0;
             for (int wd = cj * wpc + lane; wd < min(words, (cj + 1) * wpc); wd += 32) {
               cp += __popc(bitmap[wd]);
+              if (dst) dst[wd - cj * wpc] = bitmap[wd];
               bitmap[wd] = 0;
             }
+            // a chunk cut by the row's last column: the rest of its words are empty
+            if (dst)
+              for (int wd = max(words, cj * wpc) + lane; wd < (cj + 1) * wpc; wd += 32) dst[wd - cj * wpc] = 0u;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) cp += __shfl_xor_sync(0xffffffffu, cp, o);
             if (lane == 0 && cp) dcnt[(lo >> shift) + cj] += cp;

@@ -114,9 +114,13 @@ struct magnus_ctx {
   int64_t* hinter = nullptr;
   uint32_t* ce = nullptr;     // chunk tables: element prefix / distinct-column prefix
   uint32_t* cd = nullptr;
+  uint32_t* cbm_slot = nullptr;   // per chunk entry: slot of its column bitmap in cbm_pool (big chunks)
+  uint32_t* cbm_pool = nullptr;
+  uint64_t cbm_cap = 0;
   std::vector<int64_t> h_hinter, h_nent;
-  cudaStream_t aux = nullptr;   // second stream for independent reducers
+  cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr;   // concurrent pipelines
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_e[2] = {nullptr, nullptr}, ev_r[2] = {nullptr, nullptr}, ev_b[2] = {nullptr, nullptr};
   int64_t host_stats[mg::kStatLen] = {0};
   int64_t coarse_batches = 0;
   mg::Sem sem{};
@@ -130,7 +134,7 @@ struct magnus_ctx {
     if (!event_pool.empty()) { cudaEvent_t e = event_pool.back(); event_pool.pop_back(); return e; }
     cudaEvent_t e; cudaEventCreate(&e); return e;
   }
-  // bracket one launch: call begin() before and end() after
+  // bracket one launch: call begin() before and end() after (on the launch's stream)
   int pending = -1; cudaEvent_t pend_a = nullptr;
   void begin(int kernel) {
     ++launches;
@@ -144,6 +148,21 @@ struct magnus_ctx {
     cudaEventRecord(b, stream);
     marks.push_back({pending, pend_a, b});
     pending = -1;
+  }
+  // the same for a launch on another stream (concurrent pipelines)
+  cudaEvent_t begin_on(int kernel, cudaStream_t st) {
+    ++launches;
+    if (!profile) return nullptr;
+    cudaEvent_t a = get_event();
+    cudaEventRecord(a, st);
+    (void)kernel;
+    return a;
+  }
+  void end_on(int kernel, cudaEvent_t a, cudaStream_t st) {
+    if (!profile || !a) return;
+    cudaEvent_t b = get_event();
+    cudaEventRecord(b, st);
+    marks.push_back({kernel, a, b});
   }
 
   void free_all() {
@@ -263,8 +282,15 @@ int magnus_ctx_create(magnus_ctx** out) {
                                (int)mg::bin_big_smem(mg::kBinMaxShift)));
 
   MG_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+  MG_CUDA(cudaStreamCreateWithFlags(&c->aux2, cudaStreamNonBlocking));
+  MG_CUDA(cudaStreamCreateWithFlags(&c->aux3, cudaStreamNonBlocking));
   MG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   MG_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  for (int q = 0; q < 2; ++q) {
+    MG_CUDA(cudaEventCreateWithFlags(&c->ev_e[q], cudaEventDisableTiming));
+    MG_CUDA(cudaEventCreateWithFlags(&c->ev_r[q], cudaEventDisableTiming));
+    MG_CUDA(cudaEventCreateWithFlags(&c->ev_b[q], cudaEventDisableTiming));
+  }
   *out = c;
   return MAGNUS_OK;
 }
@@ -276,6 +302,13 @@ void magnus_ctx_destroy(magnus_ctx* ctx) {
   for (auto& m : ctx->marks) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->aux2) cudaStreamDestroy(ctx->aux2);
+  if (ctx->aux3) cudaStreamDestroy(ctx->aux3);
+  for (int q = 0; q < 2; ++q) {
+    if (ctx->ev_e[q]) cudaEventDestroy(ctx->ev_e[q]);
+    if (ctx->ev_r[q]) cudaEventDestroy(ctx->ev_r[q]);
+    if (ctx->ev_b[q]) cudaEventDestroy(ctx->ev_b[q]);
+  }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   delete ctx;
@@ -452,6 +485,16 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     MG_CUDA(cudaStreamSynchronize(s));
     MG_CUDA(ctx->alloc(&ctx->ce, total_ent));
     MG_CUDA(ctx->alloc(&ctx->cd, total_ent));
+    // column bitmaps of big chunks (> kBinE elements), written by the symbolic pass: at most
+    // sum(inter) / (kBinE + 1) of them; the pool is capped (chunks beyond it are marked again)
+    if (ctx->gshift == ctx->sem.shift_num && ctx->sem.shift_num >= 10) {
+      int64_t tot_inter = 0;
+      for (int64_t h = 0; h < nH; ++h) tot_inter += ctx->h_hinter[h];
+      const int64_t wpc = int64_t(1) << (ctx->sem.shift_num - 5);
+      ctx->cbm_cap = (uint64_t)std::min<int64_t>(tot_inter / (mg::kBinE + 1) + 1, (int64_t(4) << 30) / (wpc * 4));
+      MG_CUDA(ctx->alloc(&ctx->cbm_slot, total_ent));
+      MG_CUDA(ctx->alloc(&ctx->cbm_pool, (size_t)ctx->cbm_cap * wpc));
+    }
   }
   ctx->ready = true;
   return MAGNUS_OK;
@@ -484,7 +527,10 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     if (reserved > used) free_b += (size_t)(reserved - used);
   }
   const int64_t per_elem = 10;   // u16 local column + f64 product
-  int64_t cap = std::min<int64_t>(total, std::min<int64_t>((int64_t)(free_b * 0.4) / per_elem, int64_t(3) << 30));
+  int64_t cap = std::min<int64_t>(total, std::min<int64_t>((int64_t)(free_b * 0.2) / per_elem, int64_t(3) << 30));
+#ifdef MG_CAP_ELEMS
+  cap = std::min<int64_t>(cap, MG_CAP_ELEMS);
+#endif
   cap = std::max(cap, max_row);
   // batches [h0, h1) and the largest chunk-table span of a batch
   std::vector<int64_t> cuts{0};
@@ -508,19 +554,19 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
       buf_elems = std::max(buf_elems, a);
     }
   }
-  void *bcol = nullptr, *bval = nullptr, *items = nullptr, *cnts = nullptr;
-  MG_CUDA(cudaMallocAsync(&bcol, (size_t)std::max<int64_t>(buf_elems, 1) * 2, s));
-  MG_CUDA(cudaMallocAsync(&bval, (size_t)std::max<int64_t>(buf_elems, 1) * 8, s));
-  // windows and units: <= one per chunk entry; big-chunk parts: <= entries + elements / kBigSplit
+  // two buffer sets: the expand of batch b+1 overlaps the reducers of batch b
+  const int nbuf = cuts.size() > 2 ? 2 : 1;
   const int64_t max_big = std::max<int64_t>(max_ent, 1) + buf_elems / mg::kBigSplit + 1;
-  MG_CUDA(cudaMallocAsync(&items, ((size_t)std::max<int64_t>(max_ent, 1) * 2 + (size_t)max_big) * sizeof(mg::BinItem), s));
-  MG_CUDA(cudaMallocAsync(&cnts, 64, s));
-  mg::BinItem* wins = static_cast<mg::BinItem*>(items);
-  mg::BinItem* units = wins + std::max<int64_t>(max_ent, 1);
-  mg::BinItem* bigs = units + std::max<int64_t>(max_ent, 1);
-  auto* nwin = static_cast<unsigned long long*>(cnts);
-  auto* nunit = nwin + 1;
-  auto* nbig = nwin + 2;
+  void *bcol[2] = {nullptr, nullptr}, *bval[2] = {nullptr, nullptr}, *items[2] = {nullptr, nullptr},
+       *cnts[2] = {nullptr, nullptr};
+  for (int q = 0; q < nbuf; ++q) {
+    // (+64 bytes: bulk copies read 16-byte aligned supersets of a slice)
+    MG_CUDA(cudaMallocAsync(&bcol[q], (size_t)std::max<int64_t>(buf_elems, 1) * 2 + 64, s));
+    MG_CUDA(cudaMallocAsync(&bval[q], (size_t)std::max<int64_t>(buf_elems, 1) * 8 + 64, s));
+    // windows and units: <= one per chunk entry; big-chunk parts: <= entries + elements / kBigSplit
+    MG_CUDA(cudaMallocAsync(&items[q], ((size_t)std::max<int64_t>(max_ent, 1) * 2 + (size_t)max_big) * sizeof(mg::BinItem), s));
+    MG_CUDA(cudaMallocAsync(&cnts[q], 64, s));
+  }
   const size_t big_smem = mg::bin_big_smem(ctx->sem.shift_num);
   int occ_b = 1;
   MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, mg::k_bin_big, 32, big_smem));
@@ -538,13 +584,27 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
       if (h < nH) a += ctx->h_hinter[h];
     }
   }
+  cudaStream_t sr = ctx->aux, sbig = ctx->aux2;
+  bool used[2] = {false, false};
   for (size_t b = 0; b + 1 < cuts.size(); ++b) {
+    const int q = (int)(b % nbuf);
     const int64_t h0 = cuts[b], h1 = cuts[b + 1];
-    MG_CUDA(cudaMemsetAsync(cnts, 0, 64, s));
+    mg::BinItem* wins = static_cast<mg::BinItem*>(items[q]);
+    mg::BinItem* units = wins + std::max<int64_t>(max_ent, 1);
+    mg::BinItem* bigs = units + std::max<int64_t>(max_ent, 1);
+    auto* nwin = static_cast<unsigned long long*>(cnts[q]);
+    auto* nunit = nwin + 1;
+    auto* nbig = nwin + 2;
+    if (used[q]) {   // the reducers of batch b - nbuf still read this buffer set
+      MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_r[q], 0));
+      MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_b[q], 0));
+    }
+    used[q] = true;
+    MG_CUDA(cudaMemsetAsync(cnts[q], 0, 64, s));
     ctx->begin(MAGNUS_K_BIN_PLAN);
     mg::k_bin_plan<<<(unsigned)std::min<int64_t>((h1 - h0 + 7) / 8, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
         ctx->listH, h0, h1, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, wins, nwin, bigs, nbig, units,
-        nunit);
+        nunit, std::max<int64_t>(max_ent, 1), max_big);
     ctx->end();
     ctx->begin(MAGNUS_K_BIN_EXPAND);
 #ifndef MG_EXP_CTAS
@@ -552,40 +612,61 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
 #endif
     mg::k_bin_expand<<<(unsigned)(ctx->sm_count * std::min(occ_e, MG_EXP_CTAS)), mg::kBinT, 0, s>>>(
         ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
-        nunit, nwin + 3, static_cast<uint16_t*>(bcol), static_cast<double*>(bval));
+        nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]));
     ctx->end();
-    // the big-chunk and small-chunk reducers are independent: run them side by side
-    // (profiled together as MAGNUS_K_BIN_REDUCE)
-    ctx->begin(MAGNUS_K_BIN_REDUCE);
-    MG_CUDA(cudaEventRecord(ctx->ev_fork, s));
-    MG_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
-    mg::k_bin_big<<<(unsigned)(ctx->sm_count * occ_b), 32, big_smem, ctx->aux>>>(
-        ctx->listH, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->hbase, hb[b], bigs, nbig, nwin + 5,
-        static_cast<const uint16_t*>(bcol), static_cast<const double*>(bval), c_rp, c_col, c_val, ctx->err);
-    ++ctx->launches;
-    MG_CUDA(cudaEventRecord(ctx->ev_join, ctx->aux));
-    mg::k_bin_reduce<<<(unsigned)(ctx->sm_count * occ), mg::kBinT, red_smem, s>>>(
+    MG_CUDA(cudaEventRecord(ctx->ev_e[q], s));
+    // the big-chunk and small-chunk reducers of this batch run on their own streams
+    MG_CUDA(cudaStreamWaitEvent(sbig, ctx->ev_e[q], 0));
+    cudaEvent_t m1 = ctx->begin_on(MAGNUS_K_BIN_BIG, sbig);
+    mg::k_bin_big<<<(unsigned)(ctx->sm_count * occ_b), 32, big_smem, sbig>>>(
+        ctx->listH, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->hbase, hb[b], bigs, nbig, nwin + 5, max_big,
+        ctx->cbm_pool, ctx->cbm_slot, static_cast<const uint16_t*>(bcol[q]), static_cast<const double*>(bval[q]), c_rp, c_col, c_val, ctx->err);
+    ctx->end_on(MAGNUS_K_BIN_BIG, m1, sbig);
+    MG_CUDA(cudaEventRecord(ctx->ev_b[q], sbig));
+    MG_CUDA(cudaStreamWaitEvent(sr, ctx->ev_e[q], 0));
+    cudaEvent_t m2 = ctx->begin_on(MAGNUS_K_BIN_REDUCE, sr);
+    mg::k_bin_reduce<<<(unsigned)(ctx->sm_count * occ), mg::kBinT, red_smem, sr>>>(
         ctx->listH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->hbase, hb[b], wins, nwin,
-        nwin + 4, static_cast<const uint16_t*>(bcol), static_cast<const double*>(bval), c_rp, c_col, c_val, ctx->err);
-    MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_join, 0));
-    ctx->end();
+        nwin + 4, static_cast<const uint16_t*>(bcol[q]), static_cast<const double*>(bval[q]), c_rp, c_col, c_val, ctx->err);
+    ctx->end_on(MAGNUS_K_BIN_REDUCE, m2, sr);
+    MG_CUDA(cudaEventRecord(ctx->ev_r[q], sr));
     MG_CUDA(cudaGetLastError());
   }
-  MG_CUDA(cudaFreeAsync(bcol, s));
-  MG_CUDA(cudaFreeAsync(bval, s));
-  MG_CUDA(cudaFreeAsync(items, s));
-  MG_CUDA(cudaFreeAsync(cnts, s));
+  for (int q = 0; q < nbuf; ++q) {
+    if (!used[q]) continue;
+    MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_r[q], 0));
+    MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_b[q], 0));
+  }
+  for (int q = 0; q < nbuf; ++q) {
+    MG_CUDA(cudaFreeAsync(bcol[q], s));
+    MG_CUDA(cudaFreeAsync(bval[q], s));
+    MG_CUDA(cudaFreeAsync(items[q], s));
+    MG_CUDA(cudaFreeAsync(cnts[q], s));
+  }
   return MAGNUS_OK;
 }
 
+static int launch_light(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint32_t* c_col, double* c_val);
+
 static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint32_t* c_col, double* c_val) {
   cudaStream_t s = ctx->stream;
-  const int64_t nW = ctx->host_stats[mg::kStatNW], nB = ctx->host_stats[mg::kStatNB], nH = ctx->host_stats[mg::kStatNH];
+  const int64_t nH = ctx->host_stats[mg::kStatNH];
+  // the light row classes run on a side stream, concurrently with the heavy rows
+  const bool side = nH > 0;
+  if (side) {
+    MG_CUDA(cudaEventRecord(ctx->ev_fork, s));
+    MG_CUDA(cudaStreamWaitEvent(ctx->aux3, ctx->ev_fork, 0));
+    ctx->stream = ctx->aux3;
+  }
+  int rc = launch_light(ctx, numeric, c_rp, c_col, c_val);
+  ctx->stream = s;
+  if (rc) return rc;
+  if (side) MG_CUDA(cudaEventRecord(ctx->ev_join, ctx->aux3));
   if (nH > 0 && numeric && ctx->binned) {
     int rc = launch_binned(ctx, c_rp, c_col, c_val);
     if (rc) return rc;
   } else if (nH > 0) {
-    MG_CUDA(cudaMemsetAsync(ctx->work, 0, 8, s));
+    MG_CUDA(cudaMemsetAsync(ctx->work, 0, 24, s));
     const unsigned grid = (unsigned)std::min<int64_t>(nH, numeric ? 2 * ctx->sm_count : ctx->sm_count);
     ctx->begin(numeric ? MAGNUS_K_NUM_HEAVY : MAGNUS_K_SYM_HEAVY);
     if (numeric)
@@ -595,10 +676,18 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
     else
       mg::k_heavy_symbolic<<<grid, mg::kHT, mg::HeavySymSmem::kTotal, s>>>(
           ctx->A, ctx->B, ctx->listH, nH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->counts, ctx->modebits, ctx->gk,
-          ctx->gk_stride, ctx->gchunk, ctx->work, ctx->binned ? 1 : 0, ctx->ncnt, ctx->choff, ctx->ce, ctx->cd);
+          ctx->gk_stride, ctx->gchunk, ctx->work, ctx->binned ? 1 : 0, ctx->ncnt, ctx->choff, ctx->ce, ctx->cd,
+          ctx->cbm_pool, ctx->cbm_slot, ctx->cbm_cap);
     ctx->end();
     MG_CUDA(cudaGetLastError());
   }
+  if (side) MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+  return MAGNUS_OK;
+}
+
+static int launch_light(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint32_t* c_col, double* c_val) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nW = ctx->host_stats[mg::kStatNW], nB = ctx->host_stats[mg::kStatNB];
   if (nB > 0) {
     const unsigned grid = (unsigned)std::min<int64_t>(nB, (int64_t)ctx->sm_count * 3);
     ctx->begin(numeric ? MAGNUS_K_NUM_BLOCK : MAGNUS_K_SYM_BLOCK);
@@ -699,6 +788,17 @@ int magnus_numeric(magnus_ctx* ctx, const int64_t* c_row_ptr, uint32_t* c_col, d
     counters->rows_fine = ctx->host_stats[mg::kStatCat + 2];
     counters->rows_coarse = ctx->host_stats[mg::kStatCat + 3];
   }
+  return MAGNUS_OK;
+}
+
+// internal debug hook: counters of the big-chunk reducer when built with -DMG_BIG_STATS
+int magnus_debug_big_stats(unsigned long long* out8) {
+#ifdef MG_BIG_STATS
+  MG_CUDA(cudaDeviceSynchronize());
+  MG_CUDA(cudaMemcpyFromSymbol(out8, mg::g_big_stats, 8 * 8));
+#else
+  for (int i = 0; i < 8; ++i) out8[i] = 0;
+#endif
   return MAGNUS_OK;
 }
 

@@ -28,7 +28,11 @@ for r in range(reps):
     rp = plan.symbolic()
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    C, counters = plan.numeric(rp)
+    try:
+        C, counters = plan.numeric(rp)
+    except Exception as ex:   # timing-only variants may break the result
+        print("numeric:", type(ex).__name__)
+        C = None
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     prof = plan.ctx.profile_read()
