@@ -134,3 +134,47 @@ def test_heavy_paths_by_crossover(crossover):
         for sysp in (B200, FINE4K):
             ref = oracle.spgemm(A, B, sysp, thresholds=th)
             assert_same(spgemm_magnus(A, B, sys=sysp, thresholds=th), ref)
+
+
+def _hot_chunk_matrix(seed=11):
+    """Rows whose products pile into single chunks (2^20 columns): one row with ~220K
+    products inside columns [0, 4096) -- more than one big-chunk reducer part --, rows
+    with mid-size hot chunks, and light rows."""
+    rng = np.random.default_rng(seed)
+    m, n = 1 << 12, 1 << 20
+    rows = []
+    for i in range(m):
+        if i == 0:
+            r = np.arange(1, 1 + 220)                        # 220 k's ...
+        elif i < 40:
+            r = rng.choice(20000, size=int(rng.integers(20, 200)), replace=False)
+        else:
+            r = rng.choice(20000, size=int(rng.integers(1, 9)), replace=False)
+        rows.append(np.unique(r))
+    B_rows = []
+    for k in range(20000):                                  # rows >= 20000 of B are empty
+        if 1 <= k <= 220:                                   # ... each B row dense in columns [0, 4096)
+            B_rows.append(rng.choice(4096, size=1000, replace=False))
+        elif k < 2000:
+            B_rows.append(rng.choice(1 << 15, size=int(rng.integers(50, 400)), replace=False))
+        else:
+            B_rows.append(rng.choice(n, size=int(rng.integers(1, 16)), replace=False))
+
+    def csr(rr, nrows, nc, seedv):
+        rr = [np.unique(r) for r in rr]
+        rp = np.zeros(nrows + 1, np.int64)
+        np.cumsum([len(r) for r in rr], out=rp[1:len(rr) + 1])
+        rp[len(rr) + 1:] = rp[len(rr)]
+        col = np.concatenate(rr).astype(np.int32)
+        val = generate.uniform_pm1(seedv, 0xCD, np.arange(col.size, dtype=np.uint64))
+        return CsrMatrix(nrows, nc, rp, col, val)
+
+    return csr(rows, m, n, seed), csr(B_rows, n, n, seed + 1)
+
+
+@pytest.mark.parametrize("sysname", ["b200", "fine4k"])
+def test_hot_chunks_against_oracle(sysname):
+    A, B = _hot_chunk_matrix()
+    sysp = {"b200": B200, "fine4k": FINE4K}[sysname]
+    ref = oracle.spgemm(A, B, sysp)
+    assert_same(spgemm_magnus(A, B, sys=sysp), ref)
