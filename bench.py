@@ -304,6 +304,15 @@ def main():
     if dom_bytes is not None:
         dom_bytes = dom_bytes // nl_dom   # the class's bytes are split over its launches (row batches)
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_bytes else None
+    # DRAM traffic per launch of that kernel from the committed ncu capture of this workload
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                         "r1_traffic_cfg3.json")))
+        if cfg == 3 and world == 1 and dom in tj["kernels"]:
+            traffic = tj["kernels"][dom]["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        traffic = None
     prof_share = {k: round(v[0], 3) for k, v in prof.items() if v[1]}
 
     # whole-job compulsory roofline
@@ -350,7 +359,9 @@ def main():
                               "frac": round(comp / (ms_step * 1e-3) / 1e9 / (peak * world), 4), "unit": "GB/s"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4) if achieved else None, "traffic": None,
+                         "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
+                         "traffic_source": "profiles/r1_traffic_cfg3.txt (ncu dram__bytes_read+write, mean per launch)"
+                         if traffic else None,
                          "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4)},
             "kernel_ms": prof_share,
             "e2e": e2e,

@@ -43,7 +43,10 @@ constexpr int kBinWinT = kBinE / 2;   // window packing quantum
 constexpr int kBinMaxShift = 14;      // chunk width <= 16384 columns (u16 chunk-local columns)
 constexpr int kSubShift = 14;         // table granularity (sub-bin == chunk while shift_num <= 14)
 constexpr int kBinCur = 1024;         // expand: chunk cursors per warp (shared memory)
-constexpr int64_t kBinUnitMax = 1 << 17;   // expand: elements per unit (rows above are split by chunk ranges)
+#ifndef MG_UNIT_MAX
+#define MG_UNIT_MAX (1 << 17)
+#endif
+constexpr int64_t kBinUnitMax = MG_UNIT_MAX;   // expand: elements per unit (rows above are split by chunk ranges)
 #ifndef MG_EXP_U
 #define MG_EXP_U 8
 #endif
@@ -588,7 +591,10 @@ constexpr int kBigD = MG_BIG_D;            // ranks accumulated per pass
 #define MG_BIG_RS 3
 #endif
 constexpr int kBigRunSer = MG_BIG_RS;      // waves with fewer run breaks are applied run by run
-constexpr int kBigNS = 4;                  // ring stages per warp
+#ifndef MG_BIG_NS
+#define MG_BIG_NS 2
+#endif
+constexpr int kBigNS = MG_BIG_NS;          // ring stages per warp
 constexpr int kBigSE = 256;                // elements per stage
 constexpr int kBigSC = kBigSE * 2 + 16;    // stage bytes: columns (+ alignment slack)
 constexpr int kBigSV = kBigSE * 8 + 16;    // stage bytes: values (+ alignment slack)
