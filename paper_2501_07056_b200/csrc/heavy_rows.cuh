@@ -42,10 +42,23 @@ constexpr int kNT = 512;                // numeric: threads per CTA (2 CTAs / SM
 constexpr int kCap = 4096;              // numeric: stream elements per batch
 constexpr int kItems = kCap / kNT;      // 16 stream elements per thread per batch
 constexpr int kSymItems = 16;           // symbolic: stream elements per thread per tile
-constexpr int kKS = 1024;               // symbolic: k's whose cursors live in shared memory
+#ifndef MG_SYM_KS
+#define MG_SYM_KS 512
+#endif
+#ifndef MG_SYM_WINLOG
+#define MG_SYM_WINLOG 19
+#endif
+#ifndef MG_SYM_CHUNK
+#define MG_SYM_CHUNK 2048
+#endif
+#ifndef MG_SYM_CTAS
+#define MG_SYM_CTAS 2
+#endif
+constexpr int kSymCtas = MG_SYM_CTAS;   // symbolic: CTAs per SM
+constexpr int kKS = MG_SYM_KS;          // symbolic: k's whose cursors live in shared memory
 constexpr int kKSN = 256;               // numeric: k's whose cursors live in shared memory
-constexpr int kSymWin = 1 << 20;        // symbolic window width (columns; 128 KB bitmap)
-constexpr int kChunkSmem = 8192;        // numeric-plan chunk counters kept in smem (symbolic)
+constexpr int kSymWin = 1 << MG_SYM_WINLOG;   // symbolic window width (columns; 64 KB bitmap)
+constexpr int kChunkSmem = MG_SYM_CHUNK;      // numeric-plan chunk / bin counters kept in smem (symbolic)
 
 // Conflict-free in-place exclusive scan of a[0..n): each warp owns a contiguous
 // slice walked 32 entries at a time (lane-consecutive addresses).
@@ -187,10 +200,10 @@ struct HeavySymSmem {
   static constexpr size_t kScratch = 64 * 8;
   static constexpr size_t kTotal = kBitmap + kChunk + kK + kScratch;
   static_assert(kBitmap % 16 == 0 && kChunk % 16 == 0 && kK % 16 == 0, "16-byte aligned sections");
-  static_assert(kTotal + 64 <= 232448, "fits the opt-in shared memory of one CTA");
+  static_assert(kTotal + 64 <= 232448 / kSymCtas - 1024, "kSymCtas CTAs fit one SM's shared memory");
 };
 
-__global__ void __launch_bounds__(kHT, 1)
+__global__ void __launch_bounds__(kHT, kSymCtas)
 k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows, const int8_t* __restrict__ cat,
                  const int64_t* __restrict__ mn, const int64_t* __restrict__ mx, Sem sem, int64_t* __restrict__ counts,
                  uint32_t* __restrict__ modebits, uint32_t* __restrict__ gk, int64_t gk_stride,

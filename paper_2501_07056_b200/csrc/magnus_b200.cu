@@ -456,8 +456,9 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   ctx->gshift = mg::bin_shift_of(ctx->sem.shift_num);
   ctx->ncnt = ctx->binned ? (ctx->plan_num.plan_cols >> ctx->gshift) : n_chunks_global;
   const bool chunk_global = ctx->ncnt > mg::kChunkSmem;
-  MG_CUDA(ctx->alloc(&ctx->gchunk, chunk_global ? (size_t)ctx->sm_count * ctx->ncnt * 2 : 1));
-  if (chunk_global) MG_CUDA(cudaMemsetAsync(ctx->gchunk, 0, (size_t)ctx->sm_count * ctx->ncnt * 8, s));
+  const size_t gchunk_n = (size_t)ctx->sm_count * mg::kSymCtas * ctx->ncnt * 2;
+  MG_CUDA(ctx->alloc(&ctx->gchunk, chunk_global ? gchunk_n : 1));
+  if (chunk_global) MG_CUDA(cudaMemsetAsync(ctx->gchunk, 0, gchunk_n * 4, s));
   MG_CUDA(ctx->alloc(&ctx->counts, n + 1));
   MG_CUDA(ctx->alloc(&ctx->tile_sums, (n + mg::kScanTile - 1) / mg::kScanTile + 1));
   if (ctx->binned) {
@@ -667,7 +668,7 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
     if (rc) return rc;
   } else if (nH > 0) {
     MG_CUDA(cudaMemsetAsync(ctx->work, 0, 24, s));
-    const unsigned grid = (unsigned)std::min<int64_t>(nH, numeric ? 2 * ctx->sm_count : ctx->sm_count);
+    const unsigned grid = (unsigned)std::min<int64_t>(nH, (int64_t)ctx->sm_count * (numeric ? 2 : mg::kSymCtas));
     ctx->begin(numeric ? MAGNUS_K_NUM_HEAVY : MAGNUS_K_SYM_HEAVY);
     if (numeric)
       mg::k_heavy_numeric<<<grid, mg::kNT, mg::HeavyNumSmem::kTotal, s>>>(
