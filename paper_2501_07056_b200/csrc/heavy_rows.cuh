@@ -273,14 +273,32 @@ k_heavy_symbolic(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t n
         const uint32_t q0 = t0 + threadIdx.x * kSymItems;
         if (q0 < S) {
           int t = kstate_find(st, nk, q0);
+          // consecutive elements mostly share a bitmap word and a chunk: combine in
+          // registers, one shared-memory atomic per change
+          uint32_t wword = 0xffffffffu, wbits = 0, cchunk = 0xffffffffu, ccount = 0;
           for (uint32_t q = q0; q < min(S, q0 + kSymItems); ++q) {
             while (st.koff[t + 1] <= q) ++t;
             const uint32_t pos = st.ks[t] + (q - st.koff[t]);
             const uint32_t c = __ldg(B.col + pos);
             const uint32_t lc = (uint32_t)(c - lo);
-            atomicOr(&bitmap[lc >> 5], 1u << (lc & 31));
-            if (need_counts) atomicAdd(&ccnt[c >> shift], 1u);
+            if ((lc >> 5) != wword) {
+              if (wbits) atomicOr(&bitmap[wword], wbits);
+              wword = lc >> 5;
+              wbits = 0;
+            }
+            wbits |= 1u << (lc & 31);
+            if (need_counts) {
+              const uint32_t f = c >> shift;
+              if (f != cchunk) {
+                if (ccount) atomicAdd(&ccnt[cchunk], ccount);
+                cchunk = f;
+                ccount = 0;
+              }
+              ++ccount;
+            }
           }
+          if (wbits) atomicOr(&bitmap[wword], wbits);
+          if (ccount) atomicAdd(&ccnt[cchunk], ccount);
         }
       }
       __syncthreads();
