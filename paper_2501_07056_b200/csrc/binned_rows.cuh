@@ -156,9 +156,12 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
       const uint32_t pe = valid ? __ldg(e + js) : 0u, pi = valid ? __ldg(e + je) : 0u;
       const uint32_t n = pi - pe;
       const bool big = valid && n > (uint32_t)kBinE;
-      const bool next_big = valid && cj + 1 < rb.nchunk && (__ldg(e + rb.je(cj + 1)) - pi) > (uint32_t)kBinE;
+      // chunks above kBinWinT stand alone, so a packed window never holds more than kBinE
+      const bool next_big = valid && cj + 1 < rb.nchunk && (__ldg(e + rb.je(cj + 1)) - pi) > (uint32_t)kBinWinT;
       // ---- reduce windows: runs of small chunks; each sub-bin of a big chunk alone
-      const bool cut = valid && (cj == rb.nchunk - 1 || big || next_big || pe / kBinWinT != pi / kBinWinT);
+      // (windows also end every kBinWinT chunks: the direct reducer keeps a cursor per chunk)
+      const bool cut = valid && (cj == rb.nchunk - 1 || n > (uint32_t)kBinWinT || next_big || pe / kBinWinT != pi / kBinWinT ||
+                                 ((cj + 1) % kBinWinT) == 0);
       const uint32_t cm = __ballot_sync(0xffffffffu, cut);
       {
         const uint32_t prev = cm & lanemask_lt();
@@ -441,7 +444,7 @@ __device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* __restrict__ s
   const int lane = threadIdx.x & 31;
   uint32_t cmin = 0xffffu, cmax = 0u;
   for (uint32_t q = lane; q < n; q += 32) {
-    const uint32_t c = __ldg(sc + q);
+    const uint32_t c = sc[q];   // global or shared
     S.stc[q] = (uint16_t)c;
     cmin = min(cmin, c);
     cmax = max(cmax, c);
@@ -488,7 +491,7 @@ __device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* __restrict__ s
   for (uint32_t q0 = 0; q0 < n; q0 += 32) {
     const uint32_t q = q0 + lane;
     const bool valid = q < n;
-    const double v = valid ? __ldg(sv_g + q) : 0.0;
+    const double v = valid ? sv_g[q] : 0.0;
     const uint32_t r = valid ? (uint32_t)S.stc[q] : 0x10000u + lane;
     const uint32_t pr = __shfl_up_sync(0xffffffffu, r, 1);
     const bool brk = valid && lane > 0 && r <= pr;

@@ -281,6 +281,7 @@ int magnus_ctx_create(magnus_ctx** out) {
   MG_CUDA(cudaFuncSetAttribute(mg::k_bin_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::bin_big_smem(mg::kBinMaxShift)));
 
+
   MG_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
   MG_CUDA(cudaStreamCreateWithFlags(&c->aux2, cudaStreamNonBlocking));
   MG_CUDA(cudaStreamCreateWithFlags(&c->aux3, cudaStreamNonBlocking));
