@@ -106,7 +106,7 @@ int64_t magnus_launch_count(magnus_ctx* ctx);
 enum { MAGNUS_K_ROW_STATS = 0, MAGNUS_K_CATEGORIZE, MAGNUS_K_SYM_WARP, MAGNUS_K_SYM_BLOCK, MAGNUS_K_SYM_HEAVY,
        MAGNUS_K_SCAN, MAGNUS_K_NUM_WARP, MAGNUS_K_NUM_BLOCK, MAGNUS_K_NUM_HEAVY, MAGNUS_K_SYM_DENSE,
        MAGNUS_K_NUM_DENSE, MAGNUS_K_BIN_PLAN, MAGNUS_K_BIN_EXPAND, MAGNUS_K_BIN_REDUCE,
-       MAGNUS_K_BIN_BIG, MAGNUS_K_COUNT };
+       MAGNUS_K_BIN_BIG, MAGNUS_K_DIR_INDEX, MAGNUS_K_DIR_PLAN, MAGNUS_K_DIR_NUM, MAGNUS_K_COUNT };
 int magnus_profile_enable(magnus_ctx* ctx, int enable);
 int magnus_profile_read(magnus_ctx* ctx, double* ms, int64_t* launches);
 

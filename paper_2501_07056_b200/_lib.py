@@ -74,7 +74,8 @@ EXPORTS = ["magnus_compute_chunk_plan", "magnus_ctx_create", "magnus_ctx_destroy
            "magnus_numeric", "magnus_row_stats", "magnus_categories", "magnus_launch_count", "magnus_last_error",
            "magnus_version", "magnus_profile_enable", "magnus_profile_read"]
 KERNEL_NAMES = ["row_stats", "categorize", "sym_warp", "sym_block", "sym_heavy", "scan", "num_warp", "num_block",
-                "num_heavy", "sym_dense", "num_dense", "bin_plan", "bin_expand", "bin_reduce", "bin_big"]
+                "num_heavy", "sym_dense", "num_dense", "bin_plan", "bin_expand", "bin_reduce", "bin_big", "dir_index",
+                "dir_plan", "dir_num"]
 GEN_EXPORTS = ["magnus_gen_rmat_keys", "magnus_gen_uniform_pm1", "magnus_gen_uniform_rows"]
 
 _LIB = None

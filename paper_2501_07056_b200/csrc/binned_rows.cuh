@@ -438,13 +438,17 @@ struct ReduceSmem {
 
 // Small chunk (n <= kBinE elements): stable counting sort of the slice by column rank
 // into shared memory, then one lane per column sums its run with the chunk's association.
-__device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* __restrict__ sc, const double* __restrict__ sv_g,
-                                                  uint32_t n, uint32_t m, bool seq, uint32_t colbase, const ReduceSmem& S,
+// (GlobalIn: the slice is in global memory and read through the read-only path; else it is
+// a shared-memory list and must not be: const __restrict__ loads may become ld.global.nc.)
+template <bool GlobalIn = true>
+__device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* sc, const double* sv_g,
+                                                  uint32_t n, uint32_t m, uint64_t seqmask, int mshift, uint32_t colbase,
+                                                  const ReduceSmem& S,
                                                   uint32_t* __restrict__ c_col, double* __restrict__ c_val, int64_t out) {
   const int lane = threadIdx.x & 31;
   uint32_t cmin = 0xffffu, cmax = 0u;
   for (uint32_t q = lane; q < n; q += 32) {
-    const uint32_t c = sc[q];   // global or shared
+    const uint32_t c = GlobalIn ? (uint32_t)__ldg(sc + q) : (uint32_t)sc[q];
     S.stc[q] = (uint16_t)c;
     cmin = min(cmin, c);
     cmax = max(cmax, c);
@@ -491,7 +495,7 @@ __device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* __restrict__ s
   for (uint32_t q0 = 0; q0 < n; q0 += 32) {
     const uint32_t q = q0 + lane;
     const bool valid = q < n;
-    const double v = valid ? sv_g[q] : 0.0;
+    const double v = valid ? (GlobalIn ? __ldg(sv_g + q) : sv_g[q]) : 0.0;
     const uint32_t r = valid ? (uint32_t)S.stc[q] : 0x10000u + lane;
     const uint32_t pr = __shfl_up_sync(0xffffffffu, r, 1);
     const bool brk = valid && lane > 0 && r <= pr;
@@ -515,8 +519,13 @@ __device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* __restrict__ s
   __syncwarp();
   for (uint32_t r = lane; r < m; r += 32) {
     const uint32_t s0 = r ? u16_get(S.cnt, r - 1) : 0u, e0 = u16_get(S.cnt, r);
-    c_col[out + r] = colbase + S.inv[r];
-    c_val[out + r] = seq ? sum_seq_s(S.sval, s0, e0) : sum_pairwise_s(S.sval, s0, e0);
+#ifdef MG_DIR_DEBUG
+    if (!(s0 <= e0 && e0 <= n)) { printf("sortred r %u s0 %u e0 %u n %u m %u\n", r, s0, e0, n, m); asm volatile("trap;"); }
+#endif
+    const uint32_t cl = S.inv[r];
+    c_col[out + r] = colbase + cl;
+    // association of the column's chunk: bit (cl >> mshift) of seqmask
+    c_val[out + r] = ((seqmask >> (cl >> mshift)) & 1ull) ? sum_seq_s(S.sval, s0, e0) : sum_pairwise_s(S.sval, s0, e0);
   }
   __syncwarp();
   return true;
@@ -566,11 +575,15 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
       if (n) {
         const uint32_t dj = __ldg(d + j);
         const bool seq = ci == kCatDense || (int64_t)n >= sem.crossover;
-        ok &= reduce_chunk_sort(bcol + rowbase + ej, bval + rowbase + ej, n, __ldg(d + je) - dj, seq,
+        ok &= reduce_chunk_sort(bcol + rowbase + ej, bval + rowbase + ej, n, __ldg(d + je) - dj, seq ? ~0ull : 0ull, 16,
                                 (uint32_t)((rb.b0 + j) << gs) & cwmask, S, c_col, c_val, out_row + dj);
       }
       j = je;
     }
+#ifdef MG_DIR_DEBUG
+    if (!ok && (threadIdx.x & 31) == 0)
+      printf("bin_reduce mismatch row %lld h %d ja %d jb %d\n", (long long)i, it.h, it.ja, it.jb);
+#endif
     if (!ok && (threadIdx.x & 31) == 0) atomicOr(err, 4ull);
   }
 }
@@ -721,6 +734,9 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
     }
     __syncwarp();
     if (prefix_words(bm, pref, 0, nwords) != m) {
+#ifdef MG_DIR_DEBUG
+      if (lane == 0) printf("bin_big mismatch row %lld h %d ja %d jb %d n %u m %u bslot %u\n", (long long)i, it.h, it.ja, it.jb, n, m, bslot);
+#endif
       if (lane == 0) atomicOr(err, 4ull);
       continue;
     }

@@ -55,9 +55,10 @@ template <class F>
 __device__ __noinline__ double pairwise(const F& x, int64_t off, int64_t n) {
   if (n <= 128) return pw_leaf(x, off, n);
   // explicit post-order traversal of numpy's recursion (split at n/2 rounded down to a multiple of 8)
-  int64_t so[40], sn[40];
-  double sl[40];
-  int8_t ss[40];
+  // depth: ceil(log2(n / 128)) + 1 levels (n < 2^32 on the device)
+  int64_t so[26], sn[26];
+  double sl[26];
+  int8_t ss[26];
   int top = 0;
   so[0] = off; sn[0] = n; ss[0] = 0;
   double ret = 0.0;

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -16,6 +17,7 @@
 #include "binned_rows.cuh"
 #include "common.cuh"
 #include "dense_rows.cuh"
+#include "direct_rows.cuh"
 #include "heavy_rows.cuh"
 #include "setup_kernels.cuh"
 #include "small_rows.cuh"
@@ -28,6 +30,16 @@ int set_err(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
+
+#ifdef MG_DIR_DEBUG
+#define DIR_SYNC(what)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = cudaStreamSynchronize(s);                                                \
+    fprintf(stderr, "[dir] %s: %s\n", what, cudaGetErrorString(e_));                           \
+  } while (0)
+#else
+#define DIR_SYNC(what) do { } while (0)
+#endif
 
 #define MG_CUDA(call)                                                                         \
   do {                                                                                        \
@@ -118,6 +130,15 @@ struct magnus_ctx {
   uint32_t* cbm_pool = nullptr;
   uint64_t cbm_cap = 0;
   std::vector<int64_t> h_hinter, h_nent;
+  int64_t total_ent = 0;
+  // direct heavy path (direct_rows.cuh)
+  bool direct = false;
+  int dir_wlog = 0;
+  int dir_occ = 1;
+  int64_t dir_nwin1 = 0, dir_min_len = 0, dir_nidx = 0, kst_stride = 0;
+  int32_t* bslot = nullptr;
+  uint32_t* bidx = nullptr;
+  unsigned long long* kst = nullptr;
   cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr;   // concurrent pipelines
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_e[2] = {nullptr, nullptr}, ev_r[2] = {nullptr, nullptr}, ev_b[2] = {nullptr, nullptr};
@@ -280,8 +301,16 @@ int magnus_ctx_create(magnus_ctx** out) {
                                (int)(mg::bin_reduce_warp_smem(mg::kBinMaxShift) * (mg::kBinT / 32))));
   MG_CUDA(cudaFuncSetAttribute(mg::k_bin_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::bin_big_smem(mg::kBinMaxShift)));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_dir_num, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(mg::DirSmem::kWarp * mg::kDirNW)));
 
 
+  {
+    // the pairwise summation keeps an explicit recursion stack (common.cuh)
+    size_t stack = 0;
+    MG_CUDA(cudaDeviceGetLimit(&stack, cudaLimitStackSize));
+    if (stack < 2048) MG_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, 2048));
+  }
   MG_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
   MG_CUDA(cudaStreamCreateWithFlags(&c->aux2, cudaStreamNonBlocking));
   MG_CUDA(cudaStreamCreateWithFlags(&c->aux3, cudaStreamNonBlocking));
@@ -330,6 +359,89 @@ int magnus_row_stats(const magnus_csr* A, const magnus_csr* B, int64_t* inter, i
   return MAGNUS_OK;
 }
 
+// Direct heavy path: B window index (long rows) and per-warp cursor scratch.
+static int setup_direct(magnus_ctx* ctx) {
+  cudaStream_t s = ctx->stream;
+  const mg::DevCsr& B = ctx->B;
+  ctx->dir_wlog = std::min(mg::kDirLog, (int)ctx->sem.shift_num);
+  const int64_t W = int64_t(1) << ctx->dir_wlog;
+  ctx->dir_nwin1 = (std::max<int64_t>(B.n_cols, 1) + W - 1) / W + 1;
+  unsigned long long* dbuf = nullptr;
+  MG_CUDA(ctx->alloc(&dbuf, 48));
+  MG_CUDA(cudaMemsetAsync(dbuf, 0, 48 * 8, s));
+  const unsigned g = (unsigned)std::min<int64_t>((B.n_rows + 255) / 256 + 1, (int64_t)ctx->sm_count * 8);
+  ctx->begin(MAGNUS_K_DIR_INDEX);
+  mg::k_didx_hist<<<g, 256, 0, s>>>(B, dbuf);
+  ctx->end();
+  unsigned long long hist[40];
+  MG_CUDA(cudaMemcpyAsync(hist, dbuf, sizeof hist, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  // shortest indexed row: >= kDirIdxMinLen, and the index within ~1 GB
+  const int64_t cap_bytes = int64_t(1) << 30;
+  int b = 0;
+  while ((int64_t(1) << b) < mg::kDirIdxMinLen) ++b;
+  for (;; ++b) {
+    int64_t rows_ge = 0;
+    for (int q = b; q < 40; ++q) rows_ge += (int64_t)hist[q];
+    if (rows_ge * ctx->dir_nwin1 * 4 <= cap_bytes || b >= 39) break;
+  }
+  ctx->dir_min_len = int64_t(1) << b;
+  MG_CUDA(ctx->alloc(&ctx->bslot, B.n_rows + 1));
+  ctx->begin(MAGNUS_K_DIR_INDEX);
+  mg::k_didx_slots<<<g, 256, 0, s>>>(B, ctx->dir_min_len, ctx->bslot, dbuf + 40);
+  ctx->end();
+  unsigned long long nidx = 0;
+  MG_CUDA(cudaMemcpyAsync(&nidx, dbuf + 40, 8, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  ctx->dir_nidx = (int64_t)nidx;
+  MG_CUDA(ctx->alloc(&ctx->bidx, (size_t)std::max<int64_t>(1, ctx->dir_nidx) * ctx->dir_nwin1));
+  if (nidx > 0) {
+    ctx->begin(MAGNUS_K_DIR_INDEX);
+    mg::k_didx_fill<<<(unsigned)std::min<int64_t>(((int64_t)nidx * 32 + 255) / 256, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+        B, ctx->bslot, ctx->dir_wlog, ctx->dir_nwin1, ctx->bidx);
+    ctx->end();
+    DIR_SYNC("index fill");
+    MG_CUDA(cudaGetLastError());
+  }
+  const size_t smem = mg::DirSmem::kWarp * mg::kDirNW;
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->dir_occ, mg::k_dir_num, 32 * mg::kDirNW, smem));
+  ctx->dir_occ = std::max(ctx->dir_occ, 1);
+  const int64_t maxnk = ctx->host_stats[mg::kStatMaxNk];
+  ctx->kst_stride = ((std::max<int64_t>(maxnk, 1) + 31) / 32) * 32;
+  const size_t warps = (size_t)ctx->sm_count * ctx->dir_occ * mg::kDirNW;
+  MG_CUDA(ctx->alloc(&ctx->kst, warps * (size_t)ctx->kst_stride * 2));
+  return MAGNUS_OK;
+}
+
+// Heavy rows, numeric phase, direct path.
+static int launch_direct(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, double* c_val) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nH = ctx->host_stats[mg::kStatNH];
+  const int64_t cap = std::max<int64_t>(ctx->total_ent, 1);
+  void* items = nullptr;
+  unsigned long long* cnt = nullptr;
+  MG_CUDA(cudaMallocAsync(&items, (size_t)cap * sizeof(mg::DirItem), s));
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cnt), 64, s));
+  MG_CUDA(cudaMemsetAsync(cnt, 0, 64, s));
+  ctx->begin(MAGNUS_K_DIR_PLAN);
+  mg::k_dir_plan<<<(unsigned)std::min<int64_t>((nH + 7) / 8, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+      ctx->listH, nH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, mg::kDirItem,
+      static_cast<mg::DirItem*>(items), cnt, cap);
+  ctx->end();
+  DIR_SYNC("plan");
+  ctx->begin(MAGNUS_K_DIR_NUM);
+  mg::k_dir_num<<<(unsigned)(ctx->sm_count * ctx->dir_occ), 32 * mg::kDirNW, mg::DirSmem::kWarp * mg::kDirNW, s>>>(
+      ctx->A, ctx->B, ctx->listH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->dir_wlog, ctx->choff, ctx->ce, ctx->cd,
+      static_cast<const mg::DirItem*>(items), cnt, cnt + 2, cap, ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->kst,
+      ctx->kst_stride, c_rp, c_col, c_val, ctx->err);
+  ctx->end();
+  DIR_SYNC("num");
+  MG_CUDA(cudaGetLastError());
+  MG_CUDA(cudaFreeAsync(items, s));
+  MG_CUDA(cudaFreeAsync(cnt, s));
+  return MAGNUS_OK;
+}
+
 int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, const magnus_sys* sys,
                  const magnus_thresholds* th, int force_fine_only, void* stream) {
   if (!ctx || !A || !B || !sys || !th) return set_err(MAGNUS_INPUT, "null argument");
@@ -346,6 +458,14 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   if (th->sort_dense_crossover > mg::kCap)
     return set_err(MAGNUS_INPUT, "sort_dense_crossover above the device batch capacity (" + std::to_string(mg::kCap) + ")");
   ctx->free_all();
+  // per-setup allocations are gone: no pointer may survive into this setup
+  ctx->cbm_slot = ctx->cbm_pool = nullptr;
+  ctx->cbm_cap = 0;
+  ctx->bslot = nullptr;
+  ctx->bidx = nullptr;
+  ctx->kst = nullptr;
+  ctx->ce = ctx->cd = nullptr;
+  ctx->direct = ctx->binned = false;
   ctx->stream = (cudaStream_t)stream;
   cudaStream_t s = ctx->stream;
   ctx->A = dev_csr(*A);
@@ -454,6 +574,14 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   MG_CUDA(ctx->alloc(&ctx->gk, (size_t)2 * ctx->sm_count * ctx->gk_stride * 7));
   // binned heavy path: chunk width <= 2^14 and every big chunk dense (crossover <= kBinE)
   ctx->binned = nH > 0 && ctx->sem.shift_num <= mg::kBinMaxShift && th->sort_dense_crossover <= mg::kBinE;
+  {
+    // the binned path by default; MAGNUS_HEAVY_PATH=direct selects the direct path (no reorder
+    // buffer; bit-identical results, slower on skewed inputs -- DESIGN.md)
+    const char* hp = std::getenv("MAGNUS_HEAVY_PATH");
+    const bool want_direct = hp && std::strcmp(hp, "direct") == 0;
+    ctx->direct = ctx->binned && want_direct && ctx->sem.shift_num <= mg::kDirMaxShift &&
+                  th->sort_dense_crossover <= mg::kDirList && B->n_cols < (int64_t(1) << 32);
+  }
   ctx->gshift = mg::bin_shift_of(ctx->sem.shift_num);
   ctx->ncnt = ctx->binned ? (ctx->plan_num.plan_cols >> ctx->gshift) : n_chunks_global;
   const bool chunk_global = ctx->ncnt > mg::kChunkSmem;
@@ -485,11 +613,13 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     MG_CUDA(cudaMemcpyAsync(ctx->h_nent.data(), ctx->nent, nH * 8, cudaMemcpyDeviceToHost, s));
     MG_CUDA(cudaMemcpyAsync(&total_ent, ctx->choff + nH, 8, cudaMemcpyDeviceToHost, s));
     MG_CUDA(cudaStreamSynchronize(s));
+    ctx->total_ent = total_ent;
     MG_CUDA(ctx->alloc(&ctx->ce, total_ent));
     MG_CUDA(ctx->alloc(&ctx->cd, total_ent));
     // column bitmaps of big chunks (> kBinE elements), written by the symbolic pass: at most
     // sum(inter) / (kBinE + 1) of them; the pool is capped (chunks beyond it are marked again)
-    if (ctx->gshift == ctx->sem.shift_num && ctx->sem.shift_num >= 10) {
+    // (only where the symbolic kernel writes them: chunks wider than 32 bitmap words)
+    if (!ctx->direct && ctx->gshift == ctx->sem.shift_num && ctx->sem.shift_num > 10) {
       int64_t tot_inter = 0;
       for (int64_t h = 0; h < nH; ++h) tot_inter += ctx->h_hinter[h];
       const int64_t wpc = int64_t(1) << (ctx->sem.shift_num - 5);
@@ -497,6 +627,10 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
       MG_CUDA(ctx->alloc(&ctx->cbm_slot, total_ent));
       MG_CUDA(ctx->alloc(&ctx->cbm_pool, (size_t)ctx->cbm_cap * wpc));
     }
+  }
+  if (ctx->direct) {
+    int rc2 = setup_direct(ctx);
+    if (rc2) return rc2;
   }
   ctx->ready = true;
   return MAGNUS_OK;
@@ -664,7 +798,10 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
   ctx->stream = s;
   if (rc) return rc;
   if (side) MG_CUDA(cudaEventRecord(ctx->ev_join, ctx->aux3));
-  if (nH > 0 && numeric && ctx->binned) {
+  if (nH > 0 && numeric && ctx->direct) {
+    int rc = launch_direct(ctx, c_rp, c_col, c_val);
+    if (rc) return rc;
+  } else if (nH > 0 && numeric && ctx->binned) {
     int rc = launch_binned(ctx, c_rp, c_col, c_val);
     if (rc) return rc;
   } else if (nH > 0) {
@@ -778,7 +915,12 @@ int magnus_numeric(magnus_ctx* ctx, const int64_t* c_row_ptr, uint32_t* c_col, d
   unsigned long long e = 0;
   MG_CUDA(cudaMemcpyAsync(&e, ctx->err, 8, cudaMemcpyDeviceToHost, s));
   MG_CUDA(cudaStreamSynchronize(s));
-  if (e) return set_err(MAGNUS_CONTRACT, "numeric phase count differs from the symbolic count");
+  if (e) {
+    char buf[32];
+    snprintf(buf, sizeof buf, "%llx", e);
+    // flags: 1 light rows, 2 windowed heavy rows, 4 binned heavy rows, 8 direct heavy rows
+    return set_err(MAGNUS_CONTRACT, std::string("numeric phase count differs from the symbolic count (flags 0x") + buf + ")");
+  }
   if (counters) {
     int64_t nnz = 0;
     if (ctx->A.n_rows > 0) MG_CUDA(cudaMemcpy(&nnz, c_row_ptr + ctx->A.n_rows, 8, cudaMemcpyDeviceToHost));

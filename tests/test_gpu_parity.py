@@ -178,3 +178,28 @@ def test_hot_chunks_against_oracle(sysname):
     sysp = {"b200": B200, "fine4k": FINE4K}[sysname]
     ref = oracle.spgemm(A, B, sysp)
     assert_same(spgemm_magnus(A, B, sys=sysp), ref)
+
+
+def test_heavy_rows_1024_column_chunks():
+    """R-MAT 2^15 under the B200 parameters: numeric chunks of 1024 columns (32 bitmap
+    words), where the big-chunk reducer marks its own column bitmaps."""
+    A = generate.rmat(15, 16, seed=7)
+    ref = oracle.spgemm(A, A, B200)
+    assert_same(spgemm_magnus(A, A, sys=B200), ref)
+
+
+@pytest.mark.parametrize("case", ["rmat14", "hub", "hot", "rmat15"])
+@pytest.mark.parametrize("sysname", ["b200", "fine4k"])
+def test_direct_heavy_path(case, sysname, monkeypatch):
+    """The direct heavy path (MAGNUS_HEAVY_PATH=direct, no reorder buffer) gives the same
+    bits as the reference association."""
+    monkeypatch.setenv("MAGNUS_HEAVY_PATH", "direct")
+    if case == "hot":
+        A, B = _hot_chunk_matrix()
+    elif case == "rmat15":
+        A = B = generate.rmat(15, 16, seed=7)
+    else:
+        A, B = CASES[case]()
+    sysp = {"b200": B200, "fine4k": FINE4K}[sysname]
+    ref = oracle.spgemm(A, B, sysp)
+    assert_same(spgemm_magnus(A, B, sys=sysp), ref)
