@@ -204,7 +204,8 @@ k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t
              const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce,
              const int64_t* __restrict__ hbase, int64_t batch_base, const BinItem* __restrict__ units,
              const unsigned long long* __restrict__ nunit, unsigned long long* __restrict__ ticket, int64_t cap_units,
-             uint16_t* __restrict__ bcol, double* __restrict__ bval) {
+             uint16_t* __restrict__ bcol, double* __restrict__ bval, const int32_t* __restrict__ bslot,
+             const uint32_t* __restrict__ bidx, int64_t nwin1, int ilog) {
   __shared__ uint32_t s_cur[kBinT / 32][kBinCur];
   __shared__ uint32_t s_big[kBinT / 32][kBinCur / 32];   // big-chunk flags of the unit's chunks
   const int lane = threadIdx.x & 31;
@@ -268,8 +269,17 @@ k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t
         p0 = (uint32_t)B.rp(k);
         p1 = (uint32_t)B.rp(k + 1);
         if (!it.kind) {
-          p0 = lower_bound_col(B.col, p0, p1, clo);
-          p1 = lower_bound_col(B.col, p0, p1, chi);
+          // segment of the unit's column range: one load each from the B window index
+          // (long rows; unit bounds are sub-bin aligned), else binary searches
+          const int32_t sl = __ldg(bslot + k);
+          if (sl >= 0) {
+            const uint32_t* ix = bidx + (size_t)sl * nwin1;
+            p0 = __ldg(ix + min((int64_t)(clo >> ilog), nwin1 - 1));
+            p1 = __ldg(ix + min(chi64 >> ilog, nwin1 - 1));
+          } else {
+            p0 = lower_bound_col(B.col, p0, p1, clo);
+            p1 = lower_bound_col(B.col, p0, p1, chi);
+          }
         }
       }
       const uint32_t len = p1 - p0;

@@ -21,6 +21,7 @@
 #include "heavy_rows.cuh"
 #include "setup_kernels.cuh"
 #include "small_rows.cuh"
+#include "symbolic_rows.cuh"
 
 namespace {
 
@@ -133,6 +134,7 @@ struct magnus_ctx {
   int64_t total_ent = 0;
   // direct heavy path (direct_rows.cuh)
   bool direct = false;
+  bool sym2 = false;   // heavy symbolic: k_heavy_sym2 (symbolic_rows.cuh)
   int dir_wlog = 0;
   int dir_occ = 1;
   int64_t dir_nwin1 = 0, dir_min_len = 0, dir_nidx = 0, kst_stride = 0;
@@ -301,6 +303,8 @@ int magnus_ctx_create(magnus_ctx** out) {
                                (int)(mg::bin_reduce_warp_smem(mg::kBinMaxShift) * (mg::kBinT / 32))));
   MG_CUDA(cudaFuncSetAttribute(mg::k_bin_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::bin_big_smem(mg::kBinMaxShift)));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_heavy_sym2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)mg::Sym2Smem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_dir_num, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)(mg::DirSmem::kWarp * mg::kDirNW)));
 
@@ -360,10 +364,13 @@ int magnus_row_stats(const magnus_csr* A, const magnus_csr* B, int64_t* inter, i
 }
 
 // Direct heavy path: B window index (long rows) and per-warp cursor scratch.
-static int setup_direct(magnus_ctx* ctx) {
+// B window index (direct_rows.cuh k_didx_*): for B rows of at least kDirIdxMinLen entries,
+// the position of the first column >= g << wlog for every g.  Replaces the binary searches
+// of segment bounds at window / unit boundaries by one load.
+static int setup_bidx(magnus_ctx* ctx, int wlog) {
   cudaStream_t s = ctx->stream;
   const mg::DevCsr& B = ctx->B;
-  ctx->dir_wlog = std::min(mg::kDirLog, (int)ctx->sem.shift_num);
+  ctx->dir_wlog = wlog;
   const int64_t W = int64_t(1) << ctx->dir_wlog;
   ctx->dir_nwin1 = (std::max<int64_t>(B.n_cols, 1) + W - 1) / W + 1;
   unsigned long long* dbuf = nullptr;
@@ -403,6 +410,12 @@ static int setup_direct(magnus_ctx* ctx) {
     DIR_SYNC("index fill");
     MG_CUDA(cudaGetLastError());
   }
+  return MAGNUS_OK;
+}
+
+static int setup_direct(magnus_ctx* ctx) {
+  int rc = setup_bidx(ctx, std::min(mg::kDirLog, (int)ctx->sem.shift_num));
+  if (rc) return rc;
   const size_t smem = mg::DirSmem::kWarp * mg::kDirNW;
   MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->dir_occ, mg::k_dir_num, 32 * mg::kDirNW, smem));
   ctx->dir_occ = std::max(ctx->dir_occ, 1);
@@ -582,6 +595,11 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     ctx->direct = ctx->binned && want_direct && ctx->sem.shift_num <= mg::kDirMaxShift &&
                   th->sort_dense_crossover <= mg::kDirList && B->n_cols < (int64_t(1) << 32);
   }
+  {
+    const char* sp = std::getenv("MAGNUS_HEAVY_SYMBOLIC");
+    ctx->sym2 = ctx->binned && !(sp && std::strcmp(sp, "window") == 0) &&
+                (ctx->plan_num.plan_cols >> ctx->sem.shift_num) + 1 <= mg::kS2Chunks;
+  }
   ctx->gshift = mg::bin_shift_of(ctx->sem.shift_num);
   ctx->ncnt = ctx->binned ? (ctx->plan_num.plan_cols >> ctx->gshift) : n_chunks_global;
   const bool chunk_global = ctx->ncnt > mg::kChunkSmem;
@@ -630,6 +648,9 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   }
   if (ctx->direct) {
     int rc2 = setup_direct(ctx);
+    if (rc2) return rc2;
+  } else if (ctx->binned) {
+    int rc2 = setup_bidx(ctx, ctx->gshift);   // expand units start and end on sub-bin boundaries
     if (rc2) return rc2;
   }
   ctx->ready = true;
@@ -748,7 +769,8 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
 #endif
     mg::k_bin_expand<<<(unsigned)(ctx->sm_count * std::min(occ_e, MG_EXP_CTAS)), mg::kBinT, 0, s>>>(
         ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
-        nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]));
+        nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]),
+        ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog);
     ctx->end();
     MG_CUDA(cudaEventRecord(ctx->ev_e[q], s));
     // the big-chunk and small-chunk reducers of this batch run on their own streams
@@ -812,6 +834,11 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
       mg::k_heavy_numeric<<<grid, mg::kNT, mg::HeavyNumSmem::kTotal, s>>>(
           ctx->A, ctx->B, ctx->listH, nH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->modebits, c_rp, c_col, c_val, ctx->gk,
           ctx->gk_stride, ctx->work, ctx->err);
+    else if (ctx->binned && ctx->sym2)
+      mg::k_heavy_sym2<<<(unsigned)std::min<int64_t>(nH, ctx->sm_count), mg::kS2T, mg::Sym2Smem::kTotal, s>>>(
+          ctx->A, ctx->B, ctx->listH, nH, ctx->mn, ctx->mx, (int)ctx->sem.shift_num, ctx->counts, ctx->choff, ctx->ce,
+          ctx->cd, ctx->cbm_pool, ctx->cbm_slot, ctx->cbm_cap, ctx->work, ctx->bslot, ctx->bidx, ctx->dir_nwin1,
+          ctx->dir_wlog, ctx->gk, ctx->gk_stride);
     else
       mg::k_heavy_symbolic<<<grid, mg::kHT, mg::HeavySymSmem::kTotal, s>>>(
           ctx->A, ctx->B, ctx->listH, nH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->counts, ctx->modebits, ctx->gk,

@@ -11,10 +11,11 @@ from paper_2501_07056_b200 import MagnusPlan, detect_device_params, generate  # 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 17
 ef = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 A = generate.rmat_device(scale, ef, seed=3, rp_dtype=torch.int32)
-for _ in range(2):
+for _ in range(2 if scale < 19 else 1):
     plan = MagnusPlan(A, A, sys=detect_device_params())
     rp = plan.symbolic()
     C, cnt = plan.numeric(rp)
     torch.cuda.synchronize()
     plan.close()
+    del C
 print("ok", cnt)
