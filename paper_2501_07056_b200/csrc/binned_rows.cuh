@@ -401,6 +401,243 @@ k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t
   }
 }
 
+// Expand, two-pass variant: one CTA per unit.  The unit's stream (its k segments in
+// ascending k) is split into kE2W contiguous warp ranges.  Pass 1 counts each warp's
+// products per chunk; a prefix over warps gives every warp its starting slot in every
+// chunk slice; pass 2 walks the same range again and appends products to the slices
+// (stable: warp ranges are in stream order, and inside a wave lanes are in stream order).
+// Loads are 32 consecutive B elements per wave, mostly inside one B row (no search).
+constexpr int kE2T = 256;                  // threads per CTA
+constexpr int kE2W = kE2T / 32;            // warp ranges per unit
+constexpr int kE2K = 1024;                 // k's whose segments live in shared memory
+#ifndef MG_E2_U
+#define MG_E2_U 4
+#endif
+constexpr int kE2U = MG_E2_U;              // waves in flight per warp
+struct Exp2Smem {
+  static constexpr size_t kCnt = (size_t)kE2W * kBinCur * 4;            // per warp, per chunk of the unit
+  static constexpr size_t kK = (size_t)(kE2K + 32) * (4 + 4 + 8);       // koff, kpos, kav
+  static constexpr size_t kScratch = 64 * 8;
+  static constexpr size_t kTotal = kCnt + kK + kScratch;
+};
+
+__device__ __forceinline__ void sh_red_add_pred(bool p, uint32_t addr, uint32_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q red.shared.add.u32 [%1], %2;\n}\n"
+               :: "r"((uint32_t)p), "r"(addr), "r"(v) : "memory");
+}
+
+// position q of the unit's stream -> (segment, B position); the warp keeps the segment of
+// its last position (kk, kend = first position past it, base = B position - q)
+template <class KP>
+struct E2Cursor {
+  KP koff, kpos;
+  int nk, kk;
+  uint32_t kend, base;
+  __device__ __forceinline__ void init(uint32_t q_beg) {
+    int lo = 0, hi = nk;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (koff[mid] <= q_beg) lo = mid; else hi = mid;
+    }
+    kk = lo;
+    kend = koff[kk + 1];
+    base = kpos[kk] - koff[kk];
+  }
+  // B position of this lane's q in the wave starting at q0 (warp-uniform call); seg: segment
+  // of the position; returns true when the wave may span several segments
+  __device__ __forceinline__ bool wave(uint32_t q0, uint32_t q, uint32_t q_end, uint32_t& pos, int& seg) {
+    pos = base + q;
+    seg = kk;
+    if (q0 + 31 < kend || q0 >= q_end) return false;
+    int kl = kk;
+    while (kl < nk && koff[kl + 1] <= q) ++kl;
+    pos = kpos[kl] + (q - koff[kl]);
+    seg = kl;
+    kk = __shfl_sync(0xffffffffu, kl, 31);
+    kend = koff[kk + 1];
+    base = kpos[kk] - koff[kk];
+    return true;
+  }
+};
+
+template <class KP, class KA>
+__device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA kav, int nk, uint32_t T, int shift, uint32_t cb,
+                                          uint32_t* cnt, const uint32_t* __restrict__ e, int ja, int nent,
+                                          uint16_t* __restrict__ rc, double* __restrict__ rv, uint32_t* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t L = ((T + kE2W - 1) / kE2W + 31) & ~31u;
+  const uint32_t q_beg = min(T, (uint32_t)wid * L), q_end = min(T, q_beg + L);
+  uint32_t* wc = cnt + (size_t)wid * kBinCur;
+  const uint32_t a_wc = (uint32_t)__cvta_generic_to_shared(wc);
+  const uint32_t lt = lanemask_lt(), le = lanemask_le();
+  const uint32_t cmask = (1u << shift) - 1u;
+  // ---- pass 1: products per chunk of this warp's range
+  if (q_beg < q_end) {
+    E2Cursor<KP> cur{koff, kpos, nk, 0, 0, 0};
+    cur.init(q_beg);
+    for (uint32_t q00 = q_beg; q00 < q_end; q00 += 32 * kE2U) {
+      uint32_t cw[kE2U];
+#pragma unroll
+      for (int u = 0; u < kE2U; ++u) {
+        const uint32_t q0 = q00 + 32 * u, q = q0 + lane;
+        uint32_t pos;
+        int seg;
+        cur.wave(q0, q, q_end, pos, seg);
+        cw[u] = q < q_end ? __ldg(B.col + pos) : 0xffffffffu;
+      }
+#pragma unroll
+      for (int u = 0; u < kE2U; ++u) {
+        if (q00 + 32 * u >= q_end) break;
+        const bool valid = cw[u] != 0xffffffffu;
+        const uint32_t ch = valid ? (cw[u] >> shift) - cb : 0xffffffffu;
+        const uint32_t pch = __shfl_up_sync(0xffffffffu, ch, 1);
+        const bool head = lane == 0 || ch != pch;
+        const uint32_t hm = __ballot_sync(0xffffffffu, head);
+        const uint32_t after = hm & ~le;
+        const uint32_t nxt = after ? (uint32_t)(__ffs(after) - 1) : 32u;
+        sh_red_add_pred(valid && head, a_wc + (ch << 2), nxt - (uint32_t)lane);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- slice starts: chunk start (row-relative, from the symbolic tables) + earlier warps
+  for (int c = threadIdx.x; c < nent; c += kE2T) {
+    uint32_t run = __ldg(e + ja + c);
+#pragma unroll
+    for (int w = 0; w < kE2W; ++w) {
+      const uint32_t v = cnt[(size_t)w * kBinCur + c];
+      cnt[(size_t)w * kBinCur + c] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  // ---- pass 2: append (chunk-local column, product) to the slices
+  if (q_beg < q_end) {
+    E2Cursor<KP> cur{koff, kpos, nk, 0, 0, 0};
+    cur.init(q_beg);
+    for (uint32_t q00 = q_beg; q00 < q_end; q00 += 32 * kE2U) {
+      uint32_t cw[kE2U];
+      double vw[kE2U];
+      bool multi[kE2U];
+#pragma unroll
+      for (int u = 0; u < kE2U; ++u) {
+        const uint32_t q0 = q00 + 32 * u, q = q0 + lane;
+        uint32_t pos;
+        int seg;
+        multi[u] = cur.wave(q0, q, q_end, pos, seg);
+        cw[u] = 0xffffffffu;
+        vw[u] = 0.0;
+        if (q < q_end) {
+          cw[u] = __ldg(B.col + pos);
+          vw[u] = __dmul_rn(kav[seg], __ldg(B.val + pos));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kE2U; ++u) {
+        if (q00 + 32 * u >= q_end) break;
+        const bool valid = cw[u] != 0xffffffffu;
+        const uint32_t ch = valid ? (cw[u] >> shift) - cb : 0x40000000u + lane;
+        uint32_t rank, lastm;
+        if (!multi[u]) {
+          // one B row: equal chunks form contiguous runs
+          const uint32_t pch = __shfl_up_sync(0xffffffffu, ch, 1), nch = __shfl_down_sync(0xffffffffu, ch, 1);
+          const uint32_t hm = __ballot_sync(0xffffffffu, lane == 0 || ch != pch);
+          rank = (uint32_t)lane - (31u - __clz(hm & le));
+          lastm = __ballot_sync(0xffffffffu, lane == 31 || ch != nch);
+        } else {
+          const uint32_t peers = __match_any_sync(0xffffffffu, ch);
+          rank = __popc(peers & lt);
+          lastm = __ballot_sync(0xffffffffu, (peers >> lane) == 1u);
+        }
+        uint32_t slot = 0;
+        if (valid) slot = wc[ch] + rank;
+        __syncwarp();
+        if (valid && ((lastm >> lane) & 1u)) wc[ch] = slot + 1;
+        if (valid) {
+          rc[slot] = (uint16_t)(cw[u] & cmask);
+          rv[slot] = vw[u];
+        }
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  (void)scratch;
+}
+
+__global__ void __launch_bounds__(kE2T)
+k_bin_expand2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t* __restrict__ mn,
+              const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce,
+              const int64_t* __restrict__ hbase, int64_t batch_base, const BinItem* __restrict__ units,
+              const unsigned long long* __restrict__ nunit, unsigned long long* __restrict__ ticket, int64_t cap_units,
+              uint16_t* __restrict__ bcol, double* __restrict__ bval, const int32_t* __restrict__ bslot,
+              const uint32_t* __restrict__ bidx, int64_t nwin1, int ilog, uint32_t* __restrict__ gk, int64_t gk_stride,
+              unsigned long long* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);
+  double* s_kav = reinterpret_cast<double*>(smem + Exp2Smem::kCnt);
+  uint32_t* s_koff = reinterpret_cast<uint32_t*>(smem + Exp2Smem::kCnt + (size_t)(kE2K + 32) * 8);
+  uint32_t* s_kpos = s_koff + kE2K + 32;
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + Exp2Smem::kCnt + Exp2Smem::kK);
+  __shared__ unsigned long long s_u;
+  const uint64_t nu_front = nunit[0], nu = nu_front + nunit[5];
+  while (true) {
+    if (threadIdx.x == 0) s_u = atomicAdd(ticket, 1ull);
+    __syncthreads();
+    const unsigned long long u = s_u;
+    __syncthreads();
+    if (u >= nu) break;
+    const BinItem it = units[list_slot(u, nu_front, cap_units)];
+    const int64_t i = rows[it.h];
+    const int64_t a0 = A.rp(i);
+    const int nk = (int)(A.rp(i + 1) - a0);
+    const RowBins rb = row_bins(mn[i], mx[i], shift);   // shift <= kSubShift: entries == chunks
+    const uint32_t* e = ce + choff[it.h];
+    const int nent = it.jb - it.ja;
+    const uint32_t clo = (uint32_t)((rb.b0 + it.ja) << shift);
+    const int64_t chi64 = (rb.b0 + it.jb) << shift;
+    const uint32_t chi = chi64 >= ((int64_t)1 << 32) ? 0xffffffffu : (uint32_t)chi64;
+    const bool big_nk = nk > kE2K;
+    uint32_t* koff = big_nk ? gk + (size_t)blockIdx.x * gk_stride * 4 : s_koff;
+    uint32_t* kpos = big_nk ? koff + gk_stride : s_kpos;
+    double* kav = big_nk ? reinterpret_cast<double*>(koff + 2 * gk_stride) : s_kav;
+    for (int j = threadIdx.x; j < nk; j += kE2T) {
+      const int64_t k = __ldg(A.col + a0 + j);
+      uint32_t p0 = (uint32_t)B.rp(k), p1 = (uint32_t)B.rp(k + 1);
+      if (!it.kind) {
+        const int32_t sl = __ldg(bslot + k);
+        if (sl >= 0) {
+          const uint32_t* ix = bidx + (size_t)sl * nwin1;
+          p0 = __ldg(ix + min((int64_t)(clo >> ilog), nwin1 - 1));
+          p1 = __ldg(ix + min(chi64 >> ilog, nwin1 - 1));
+        } else {
+          p0 = lower_bound_col(B.col, p0, p1, clo);
+          p1 = lower_bound_col(B.col, p0, p1, chi);
+        }
+      }
+      koff[j] = p1 - p0;
+      kpos[j] = p0;
+      kav[j] = __ldg(A.val + a0 + j);
+    }
+    for (int c = threadIdx.x; c < kE2W * nent; c += kE2T) cnt[(c / nent) * kBinCur + (c % nent)] = 0u;
+    __syncthreads();
+    const uint32_t T = block_scan_striped<kE2T>(koff, nk, scratch);
+    if (threadIdx.x == 0) koff[nk] = T;
+    __syncthreads();
+    if (T != __ldg(e + it.jb) - __ldg(e + it.ja)) {
+      if (threadIdx.x == 0) atomicOr(err, 4ull);
+      continue;
+    }
+    const int64_t rowbase = hbase[it.h] - batch_base;
+    if (big_nk)
+      exp2_unit(B, (const uint32_t*)koff, (const uint32_t*)kpos, (const double*)kav, nk, T, shift,
+                (uint32_t)(rb.b0 + it.ja), cnt, e, it.ja, nent, bcol + rowbase, bval + rowbase, scratch);
+    else
+      exp2_unit(B, (const uint32_t*)s_koff, (const uint32_t*)s_kpos, (const double*)s_kav, nk, T, shift,
+                (uint32_t)(rb.b0 + it.ja), cnt, e, it.ja, nent, bcol + rowbase, bval + rowbase, scratch);
+  }
+}
+
 // ---------------------------------------------------------------- reduce helpers (warp scope)
 __device__ __forceinline__ uint32_t u16_get(const uint32_t* a, uint32_t r) { return (a[r >> 1] >> ((r & 1u) * 16)) & 0xffffu; }
 

@@ -146,6 +146,40 @@ __device__ int64_t block_min_i64(int64_t v, int64_t* scratch) {
   return r;
 }
 
+// Conflict-free in-place exclusive scan of a[0..n): each warp owns a contiguous
+// slice walked 32 entries at a time (lane-consecutive addresses).
+template <int T>
+__device__ uint32_t block_scan_striped(uint32_t* a, int n, uint32_t* scratch) {
+  constexpr int NW = T / 32;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int per = (((n + NW - 1) / NW) + 31) & ~31;
+  const int b = min(n, wid * per), e = min(n, b + per);
+  uint32_t s = 0;
+  for (int i = b + lane; i < e; i += 32) s += a[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) scratch[wid] = s;
+  __syncthreads();
+  if (wid == 0) {
+    const uint32_t w = lane < NW ? scratch[lane] : 0u;
+    const uint32_t wi = warp_incl_scan(w);
+    if (lane < NW) scratch[lane] = wi - w;
+    if (lane == 31) scratch[32] = wi;
+  }
+  __syncthreads();
+  uint32_t carry = scratch[wid];
+  for (int i0 = b; i0 < e; i0 += 32) {
+    const int i = i0 + lane;
+    const uint32_t v = i < e ? a[i] : 0u;
+    const uint32_t inc = warp_incl_scan(v);
+    if (i < e) a[i] = carry + inc - v;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  const uint32_t total = scratch[32];
+  __syncthreads();
+  return total;
+}
+
 // first index in [lo, hi) with col[idx] >= key (B rows are sorted: canonical input)
 __device__ __forceinline__ uint32_t lower_bound_col(const uint32_t* __restrict__ col, uint32_t lo, uint32_t hi, uint32_t key) {
   while (lo < hi) {

@@ -303,6 +303,8 @@ int magnus_ctx_create(magnus_ctx** out) {
                                (int)(mg::bin_reduce_warp_smem(mg::kBinMaxShift) * (mg::kBinT / 32))));
   MG_CUDA(cudaFuncSetAttribute(mg::k_bin_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::bin_big_smem(mg::kBinMaxShift)));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_bin_expand2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)mg::Exp2Smem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_heavy_sym2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::Sym2Smem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_dir_num, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -732,6 +734,15 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mg::k_bin_reduce, mg::kBinT, red_smem));
   int occ_e = 1;
   MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, mg::k_bin_expand, mg::kBinT, 0));
+  // two-pass CTA expand (k_bin_expand2) unless MAGNUS_EXPAND=v1
+  const char* ev = std::getenv("MAGNUS_EXPAND");
+  const bool exp2 = !(ev && std::strcmp(ev, "v1") == 0);
+  int occ_e2 = 1;
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e2, mg::k_bin_expand2, mg::kE2T, mg::Exp2Smem::kTotal));
+  occ_e2 = std::max(occ_e2, 1);
+  uint32_t* e2scr = nullptr;   // per-CTA segment tables of units with more than kE2K k's
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&e2scr),
+                          (size_t)ctx->sm_count * occ_e2 * 4 * std::max<int64_t>(ctx->gk_stride, 4) * 4, s));
   std::vector<int64_t> hb(cuts.size());
   {
     int64_t a = 0;
@@ -742,6 +753,10 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     }
   }
   cudaStream_t sr = ctx->aux, sbig = ctx->aux2;
+  // the reducers run on the main stream after each batch's expand (measured faster than
+  // overlapping them on side streams); MAGNUS_SERIAL=0 restores the concurrent pipeline
+  const char* serial_env = std::getenv("MAGNUS_SERIAL");
+  if (!(serial_env && std::strcmp(serial_env, "0") == 0)) sr = sbig = s;
   bool used[2] = {false, false};
   for (size_t b = 0; b + 1 < cuts.size(); ++b) {
     const int q = (int)(b % nbuf);
@@ -764,13 +779,20 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
         nunit, std::max<int64_t>(max_ent, 1), max_big);
     ctx->end();
     ctx->begin(MAGNUS_K_BIN_EXPAND);
+    if (exp2) {
+      mg::k_bin_expand2<<<(unsigned)(ctx->sm_count * occ_e2), mg::kE2T, mg::Exp2Smem::kTotal, s>>>(
+          ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
+          nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]),
+          ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, e2scr, ctx->gk_stride, ctx->err);
+    } else {
 #ifndef MG_EXP_CTAS
 #define MG_EXP_CTAS occ_e
 #endif
-    mg::k_bin_expand<<<(unsigned)(ctx->sm_count * std::min(occ_e, MG_EXP_CTAS)), mg::kBinT, 0, s>>>(
-        ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
-        nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]),
-        ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog);
+      mg::k_bin_expand<<<(unsigned)(ctx->sm_count * std::min(occ_e, MG_EXP_CTAS)), mg::kBinT, 0, s>>>(
+          ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
+          nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]),
+          ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog);
+    }
     ctx->end();
     MG_CUDA(cudaEventRecord(ctx->ev_e[q], s));
     // the big-chunk and small-chunk reducers of this batch run on their own streams
@@ -795,6 +817,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_r[q], 0));
     MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_b[q], 0));
   }
+  MG_CUDA(cudaFreeAsync(e2scr, s));
   for (int q = 0; q < nbuf; ++q) {
     MG_CUDA(cudaFreeAsync(bcol[q], s));
     MG_CUDA(cudaFreeAsync(bval[q], s));
@@ -810,7 +833,8 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
   cudaStream_t s = ctx->stream;
   const int64_t nH = ctx->host_stats[mg::kStatNH];
   // the light row classes run on a side stream, concurrently with the heavy rows
-  const bool side = nH > 0;
+  const char* serial_env = std::getenv("MAGNUS_SERIAL");
+  const bool side = nH > 0 && serial_env && std::strcmp(serial_env, "0") == 0;
   if (side) {
     MG_CUDA(cudaEventRecord(ctx->ev_fork, s));
     MG_CUDA(cudaStreamWaitEvent(ctx->aux3, ctx->ev_fork, 0));
