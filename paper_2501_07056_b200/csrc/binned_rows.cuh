@@ -778,6 +778,60 @@ __device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* sc, const doub
   return true;
 }
 
+// Chunk of at most 32 products (about half of all chunks of heavy rows): one product per
+// lane, sorted by (column, stream position) with a register bitonic network, runs of equal
+// columns summed with the chunk's association -- sequential from +0.0 (dense) or
+// x0 + (((-0.0 + x1) + x2) + ...) (np.add.reduceat, numpy pairwise below 8 terms).
+// Returns 1 ok, 0 count mismatch, -1 when a column has more than 8 products (the caller
+// then takes the general path).
+__device__ __forceinline__ int reduce_chunk_wave(const uint16_t* __restrict__ sc, const double* __restrict__ sv, uint32_t n,
+                                                 uint32_t m, bool seq, uint32_t colbase, uint32_t* __restrict__ c_col,
+                                                 double* __restrict__ c_val, int64_t out) {
+  const int lane = threadIdx.x & 31;
+  const bool valid = (uint32_t)lane < n;
+  uint32_t key = valid ? ((uint32_t)__ldg(sc + lane) << 5) | (uint32_t)lane : 0xffffffffu;
+  double v = valid ? __ldg(sv + lane) : 0.0;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t pk = __shfl_xor_sync(0xffffffffu, key, j);
+      const double pv = __shfl_xor_sync(0xffffffffu, v, j);
+      const bool up = (lane & k) == 0 || k == 32;
+      const bool lower = (lane & j) == 0;
+      const bool take = lower ? (up ? pk < key : pk > key) : (up ? pk > key : pk < key);
+      if (take) {
+        key = pk;
+        v = pv;
+      }
+    }
+  }
+  const uint32_t c = key >> 5;
+  const uint32_t pc = __shfl_up_sync(0xffffffffu, c, 1);
+  const bool head = valid && (lane == 0 || c != pc);
+  const uint32_t hm = __ballot_sync(0xffffffffu, head);
+  const uint32_t after = hm & ~lanemask_le();
+  const uint32_t runlen = head ? (after ? (uint32_t)(__ffs(after) - 1) : n) - (uint32_t)lane : 0u;
+  const uint32_t maxd = __reduce_max_sync(0xffffffffu, runlen);
+  if (maxd > 8u) return -1;
+  double acc = seq ? __dadd_rn(0.0, v) : v;
+  double rest = -0.0;
+  for (uint32_t t = 1; t < maxd; ++t) {
+    const double x = __shfl_sync(0xffffffffu, v, min(lane + (int)t, 31));
+    if (t < runlen) {
+      if (seq) acc = __dadd_rn(acc, x);
+      else rest = __dadd_rn(rest, x);
+    }
+  }
+  if (!seq && runlen > 1) acc = __dadd_rn(acc, rest);
+  const uint32_t rank = __popc(hm & lanemask_lt());
+  if (head) {
+    c_col[out + rank] = colbase + c;
+    c_val[out + rank] = acc;
+  }
+  return __popc(hm) == m ? 1 : 0;
+}
+
 // Reduce: one warp per window.
 __global__ void __launch_bounds__(kBinT, 8)
 k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, const int64_t* __restrict__ mn,
@@ -788,6 +842,7 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
              const double* __restrict__ bval, const int64_t* __restrict__ c_rp, uint32_t* __restrict__ c_col,
              double* __restrict__ c_val, unsigned long long* __restrict__ err) {
   extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
   const int shift = sem.shift_num, gs = bin_shift_of(shift);
   const int words = shift >= 5 ? 1 << (shift - 5) : 1;
   const size_t w4 = ((size_t)words * 4 + 15) & ~size_t(15), w2 = ((size_t)words * 2 + 15) & ~size_t(15);
@@ -815,15 +870,31 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
     const int64_t rowbase = hbase[it.h] - batch_base;
     const int64_t out_row = c_rp[i];
     bool ok = true;
+    // chunk table entries of the window, 32 chunks per load (lane l: chunk j0 + l)
+    int j0 = -1 << 30;
+    uint32_t e_l = 0, d_l = 0;
     int j = it.ja;
     while (j < it.jb) {
       const int je = (int)min((int64_t)it.jb, ((((rb.b0 + j) >> rb.cs) + 1) << rb.cs) - rb.b0);
-      const uint32_t ej = __ldg(e + j), n = __ldg(e + je) - ej;
+      if (j < j0 || je >= j0 + 32) {
+        j0 = j;
+        e_l = j0 + lane <= it.jb ? __ldg(e + j0 + lane) : 0u;
+        d_l = j0 + lane <= it.jb ? __ldg(d + j0 + lane) : 0u;
+      }
+      const uint32_t ej = __shfl_sync(0xffffffffu, e_l, j - j0), n = __shfl_sync(0xffffffffu, e_l, je - j0) - ej;
+      const uint32_t dj = __shfl_sync(0xffffffffu, d_l, j - j0), dje = __shfl_sync(0xffffffffu, d_l, je - j0);
       if (n) {
-        const uint32_t dj = __ldg(d + j);
         const bool seq = ci == kCatDense || (int64_t)n >= sem.crossover;
-        ok &= reduce_chunk_sort(bcol + rowbase + ej, bval + rowbase + ej, n, __ldg(d + je) - dj, seq ? ~0ull : 0ull, 16,
-                                (uint32_t)((rb.b0 + j) << gs) & cwmask, S, c_col, c_val, out_row + dj);
+        const uint32_t colbase = (uint32_t)((rb.b0 + j) << gs) & cwmask;
+        int r = -1;
+        if (n <= 32u)
+          r = reduce_chunk_wave(bcol + rowbase + ej, bval + rowbase + ej, n, dje - dj, seq, colbase, c_col, c_val,
+                                out_row + dj);
+        if (r < 0)
+          ok &= reduce_chunk_sort(bcol + rowbase + ej, bval + rowbase + ej, n, dje - dj, seq ? ~0ull : 0ull, 16,
+                                  colbase, S, c_col, c_val, out_row + dj);
+        else
+          ok &= r == 1;
       }
       j = je;
     }
