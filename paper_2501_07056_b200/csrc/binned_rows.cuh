@@ -407,9 +407,15 @@ k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t
 // chunk slice; pass 2 walks the same range again and appends products to the slices
 // (stable: warp ranges are in stream order, and inside a wave lanes are in stream order).
 // Loads are 32 consecutive B elements per wave, mostly inside one B row (no search).
-constexpr int kE2T = 256;                  // threads per CTA
+#ifndef MG_E2_T
+#define MG_E2_T 256
+#endif
+#ifndef MG_E2_K
+#define MG_E2_K 256
+#endif
+constexpr int kE2T = MG_E2_T;              // threads per CTA
 constexpr int kE2W = kE2T / 32;            // warp ranges per unit
-constexpr int kE2K = 1024;                 // k's whose segments live in shared memory
+constexpr int kE2K = MG_E2_K;              // k's whose segments live in shared memory
 #ifndef MG_E2_U
 #define MG_E2_U 4
 #endif

@@ -741,8 +741,8 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e2, mg::k_bin_expand2, mg::kE2T, mg::Exp2Smem::kTotal));
   occ_e2 = std::max(occ_e2, 1);
   uint32_t* e2scr = nullptr;   // per-CTA segment tables of units with more than kE2K k's
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&e2scr),
-                          (size_t)ctx->sm_count * occ_e2 * 4 * std::max<int64_t>(ctx->gk_stride, 4) * 4, s));
+  const int64_t e2_stride = ((ctx->host_stats[mg::kStatMaxNk] + 8 + 3) / 4) * 4;
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&e2scr), (size_t)ctx->sm_count * occ_e2 * 4 * e2_stride * 4, s));
   std::vector<int64_t> hb(cuts.size());
   {
     int64_t a = 0;
@@ -783,7 +783,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
       mg::k_bin_expand2<<<(unsigned)(ctx->sm_count * occ_e2), mg::kE2T, mg::Exp2Smem::kTotal, s>>>(
           ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
           nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]),
-          ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, e2scr, ctx->gk_stride, ctx->err);
+          ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, e2scr, e2_stride, ctx->err);
     } else {
 #ifndef MG_EXP_CTAS
 #define MG_EXP_CTAS occ_e
