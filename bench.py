@@ -249,6 +249,8 @@ def main():
         C, counters = plan.numeric(rp)
         launches = plan.launches()
         prof = plan.ctx.profile_read() if profile else None
+        if profile:
+            prof["_heavy"] = plan.ctx.heavy_stats()
         plan.close()
         return C, counters, launches, prof
 
@@ -285,6 +287,7 @@ def main():
 
     # kernel-level profile (one extra step, events bracket each launch on its stream)
     C, counters, _, prof = step(profile=True)
+    hs = prof.pop("_heavy")
     c_nnz_row = (C.row_ptr[1:] - C.row_ptr[:-1])
     nnz_c_local = int(C.row_ptr[-1])
     rp_a = A_loc.row_ptr.element_size()
@@ -293,7 +296,10 @@ def main():
     del C
     peak, peak_kind = hbm_peak()
     kern_bytes = {"num_heavy": ab["heavy"]["num_bytes"], "sym_heavy": ab["heavy"]["sym_bytes"],
-                  "bin_expand": ab["heavy"]["expand_bytes"], "bin_reduce": ab["heavy"]["reduce_bytes"],
+                  "bin_expand": ab["heavy"]["expand_bytes"],
+                  # reducers: the reorder buffer slices they read (10 B per product) + the C entries they write
+                  "bin_big": hs["big_products"] * 10 + hs["big_distinct"] * 12,
+                  "bin_reduce": hs["small_products"] * 10 + hs["small_distinct"] * 12,
                   "num_dense": ab["dense"]["num_bytes"], "sym_dense": ab["dense"]["sym_bytes"],
                   "num_block": ab["block"]["num_bytes"], "sym_block": ab["block"]["sym_bytes"],
                   "num_warp": ab["warp"]["num_bytes"], "sym_warp": ab["warp"]["sym_bytes"]}
@@ -308,7 +314,7 @@ def main():
     traffic = None
     try:
         tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                         "r1_traffic_cfg3.json")))
+                                         "r1_cfg3_traffic.json")))
         if cfg == 3 and world == 1 and dom in tj["kernels"]:
             traffic = tj["kernels"][dom]["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
@@ -360,10 +366,11 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
-                         "traffic_source": "profiles/r1_traffic_cfg3.txt (ncu dram__bytes_read+write, mean per launch)"
+                         "traffic_source": "profiles/r1_cfg3_traffic.json (ncu dram__bytes_read+write, mean per launch)"
                          if traffic else None,
                          "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4)},
             "kernel_ms": prof_share,
+            "heavy_chunks": hs,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clocks,

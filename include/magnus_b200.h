@@ -110,6 +110,11 @@ enum { MAGNUS_K_ROW_STATS = 0, MAGNUS_K_CATEGORIZE, MAGNUS_K_SYM_WARP, MAGNUS_K_
 int magnus_profile_enable(magnus_ctx* ctx, int enable);
 int magnus_profile_read(magnus_ctx* ctx, double* ms, int64_t* launches);
 
+/* Heavy-row telemetry after magnus_symbolic (binned / direct paths, else zeros): out[0..3] =
+ * products and distinct columns in "big" fine chunks (reduced by the dense big-chunk
+ * reducer), products and distinct columns in the other chunks (sort reducer).  Synchronises. */
+int magnus_heavy_stats(magnus_ctx* ctx, int64_t* out4);
+
 const char* magnus_last_error(void);
 const char* magnus_version(void);
 

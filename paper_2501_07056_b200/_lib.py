@@ -72,7 +72,7 @@ class Counters(C.Structure):
 # every symbol include/magnus_b200.h declares
 EXPORTS = ["magnus_compute_chunk_plan", "magnus_ctx_create", "magnus_ctx_destroy", "magnus_setup", "magnus_symbolic",
            "magnus_numeric", "magnus_row_stats", "magnus_categories", "magnus_launch_count", "magnus_last_error",
-           "magnus_version", "magnus_profile_enable", "magnus_profile_read"]
+           "magnus_version", "magnus_profile_enable", "magnus_profile_read", "magnus_heavy_stats"]
 KERNEL_NAMES = ["row_stats", "categorize", "sym_warp", "sym_block", "sym_heavy", "scan", "num_warp", "num_block",
                 "num_heavy", "sym_dense", "num_dense", "bin_plan", "bin_expand", "bin_reduce", "bin_big", "dir_index",
                 "dir_plan", "dir_num"]
@@ -106,6 +106,7 @@ def lib():
         L.magnus_gen_uniform_rows.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_uint64, C.c_void_p, C.c_void_p]
         L.magnus_profile_enable.argtypes = [C.c_void_p, C.c_int]
         L.magnus_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.magnus_heavy_stats.argtypes = [C.c_void_p, C.c_void_p]
         L.magnus_compute_chunk_plan.argtypes = [C.POINTER(Sys), C.c_int64, C.c_int, C.c_int, C.POINTER(Plan)]
         _LIB = L
     return _LIB
@@ -140,6 +141,13 @@ class Context:
 
     def profile(self, enable: bool = True) -> None:
         check(lib().magnus_profile_enable(self.h, int(enable)))
+
+    def heavy_stats(self) -> dict:
+        """Products / distinct columns of heavy rows in big chunks and in the other chunks."""
+        out = (C.c_int64 * 4)()
+        check(lib().magnus_heavy_stats(self.h, out))
+        return {"big_products": int(out[0]), "big_distinct": int(out[1]), "small_products": int(out[2]),
+                "small_distinct": int(out[3])}
 
     def profile_read(self) -> dict:
         """{kernel name: (total ms, launches)} since the last read (synchronises)."""

@@ -42,7 +42,10 @@ constexpr int kBinE = 512;            // small chunk: <= kBinE elements (sort pa
 constexpr int kBinWinT = kBinE / 2;   // window packing quantum
 constexpr int kBinMaxShift = 14;      // chunk width <= 16384 columns (u16 chunk-local columns)
 constexpr int kSubShift = 14;         // table granularity (sub-bin == chunk while shift_num <= 14)
-constexpr int kBinCur = 1024;         // expand: chunk cursors per warp (shared memory)
+#ifndef MG_BIN_CUR
+#define MG_BIN_CUR 256
+#endif
+constexpr int kBinCur = MG_BIN_CUR;   // expand: chunks per unit (cursors / counters in shared memory)
 #ifndef MG_UNIT_MAX
 #define MG_UNIT_MAX (1 << 17)
 #endif
@@ -129,6 +132,30 @@ __device__ __forceinline__ RowBins row_bins(int64_t mn, int64_t mx, int shift) {
   r.nchunk = (int)((mx >> shift) - r.c0 + 1);
   r.cs = shift - gs;
   return r;
+}
+
+// Telemetry: products / distinct columns in big (> kBinE products) and other chunks.
+__global__ void k_heavy_stats(const int32_t* __restrict__ rows, int64_t nH, const int64_t* __restrict__ mn,
+                              const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff,
+                              const uint32_t* __restrict__ ce, const uint32_t* __restrict__ cd,
+                              unsigned long long* __restrict__ out) {
+  unsigned long long pb = 0, db = 0, ps = 0, ds = 0;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t h = warp; h < nH; h += nwarps) {
+    const int64_t i = rows[h];
+    const RowBins rb = row_bins(mn[i], mx[i], shift);
+    const uint32_t* e = ce + choff[h];
+    const uint32_t* d = cd + choff[h];
+    for (int j = threadIdx.x & 31; j < rb.nb; j += 32) {
+      const uint32_t n = __ldg(e + j + 1) - __ldg(e + j), m = __ldg(d + j + 1) - __ldg(d + j);
+      if (n > (uint32_t)kBinE) { pb += n; db += m; } else { ps += n; ds += m; }
+    }
+  }
+  atomicAdd(out + 0, pb);
+  atomicAdd(out + 1, db);
+  atomicAdd(out + 2, ps);
+  atomicAdd(out + 3, ds);
 }
 
 // Windows and expand units of heavy rows [h0, h1), one warp per row.

@@ -230,6 +230,25 @@ int magnus_profile_read(magnus_ctx* ctx, double* ms, int64_t* launches) {
   return MAGNUS_OK;
 }
 
+int magnus_heavy_stats(magnus_ctx* ctx, int64_t* out4) {
+  if (!ctx || !out4) return set_err(MAGNUS_INPUT, "null argument");
+  for (int q = 0; q < 4; ++q) out4[q] = 0;
+  const int64_t nH = ctx->host_stats[mg::kStatNH];
+  if (!ctx->ready || !ctx->have_symbolic || !ctx->binned || nH == 0) return MAGNUS_OK;
+  unsigned long long* d = nullptr;
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 32, ctx->stream));
+  MG_CUDA(cudaMemsetAsync(d, 0, 32, ctx->stream));
+  mg::k_heavy_stats<<<(unsigned)std::min<int64_t>((nH + 7) / 8, (int64_t)ctx->sm_count * 8), 256, 0, ctx->stream>>>(
+      ctx->listH, nH, ctx->mn, ctx->mx, (int)ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->cd, d);
+  MG_CUDA(cudaGetLastError());
+  unsigned long long h[4];
+  MG_CUDA(cudaMemcpyAsync(h, d, 32, cudaMemcpyDeviceToHost, ctx->stream));
+  MG_CUDA(cudaFreeAsync(d, ctx->stream));
+  MG_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int q = 0; q < 4; ++q) out4[q] = (int64_t)h[q];
+  return MAGNUS_OK;
+}
+
 // compute_chunk_plan planner.py:106-152
 int magnus_compute_chunk_plan(const magnus_sys* sys, int64_t m_c, int numeric, int allow_coarse, magnus_chunk_plan* out) {
   if (!sys || !out) return set_err(MAGNUS_INPUT, "null argument");
