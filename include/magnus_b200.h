@@ -110,6 +110,12 @@ enum { MAGNUS_K_ROW_STATS = 0, MAGNUS_K_CATEGORIZE, MAGNUS_K_SYM_WARP, MAGNUS_K_
 int magnus_profile_enable(magnus_ctx* ctx, int enable);
 int magnus_profile_read(magnus_ctx* ctx, double* ms, int64_t* launches);
 
+/* magnus_numeric, and C (col, val) read back into host memory c_col_host / c_val_host (page-locked
+ * for overlap): completed row ranges are copied on a side stream while later heavy-row batches
+ * compute.  Returns after the copies have finished.  C stays on the device as well. */
+int magnus_numeric_host(magnus_ctx* ctx, const int64_t* c_row_ptr, uint32_t* c_col, double* c_val, uint32_t* c_col_host,
+                        double* c_val_host, magnus_counters* counters, void* stream);
+
 /* Heavy-row telemetry after magnus_symbolic (binned / direct paths, else zeros): out[0..3] =
  * products and distinct columns in "big" fine chunks (reduced by the dense big-chunk
  * reducer), products and distinct columns in the other chunks (sort reducer).  Synchronises. */

@@ -72,7 +72,8 @@ class Counters(C.Structure):
 # every symbol include/magnus_b200.h declares
 EXPORTS = ["magnus_compute_chunk_plan", "magnus_ctx_create", "magnus_ctx_destroy", "magnus_setup", "magnus_symbolic",
            "magnus_numeric", "magnus_row_stats", "magnus_categories", "magnus_launch_count", "magnus_last_error",
-           "magnus_version", "magnus_profile_enable", "magnus_profile_read", "magnus_heavy_stats"]
+           "magnus_version", "magnus_profile_enable", "magnus_profile_read", "magnus_heavy_stats",
+           "magnus_numeric_host"]
 KERNEL_NAMES = ["row_stats", "categorize", "sym_warp", "sym_block", "sym_heavy", "scan", "num_warp", "num_block",
                 "num_heavy", "sym_dense", "num_dense", "bin_plan", "bin_expand", "bin_reduce", "bin_big", "dir_index",
                 "dir_plan", "dir_num"]
@@ -98,6 +99,8 @@ def lib():
                                    C.c_int, C.c_void_p]
         L.magnus_symbolic.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
         L.magnus_numeric.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(Counters), C.c_void_p]
+        L.magnus_numeric_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                          C.POINTER(Counters), C.c_void_p]
         L.magnus_row_stats.argtypes = [C.POINTER(Csr), C.POINTER(Csr), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.magnus_categories.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.magnus_gen_rmat_keys.argtypes = [C.c_int, C.c_int64, C.c_int64, C.c_uint64, C.c_double, C.c_double,

@@ -162,6 +162,7 @@ __global__ void k_heavy_stats(const int32_t* __restrict__ rows, int64_t nH, cons
 __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t h1, const int64_t* __restrict__ mn,
                            const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff,
                            const uint32_t* __restrict__ ce, BinItem* __restrict__ wins, unsigned long long* __restrict__ nwin,
+                           BinItem* __restrict__ wins_t,
                            BinItem* __restrict__ bigs, unsigned long long* __restrict__ nbig, BinItem* __restrict__ units,
                            unsigned long long* __restrict__ nunit, int64_t cap_units, int64_t cap_bigs) {
   const int lane = threadIdx.x & 31;
@@ -184,17 +185,23 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
       const uint32_t n = pi - pe;
       const bool big = valid && n > (uint32_t)kBinE;
       // chunks above kBinWinT stand alone, so a packed window never holds more than kBinE
-      const bool next_big = valid && cj + 1 < rb.nchunk && (__ldg(e + rb.je(cj + 1)) - pi) > (uint32_t)kBinWinT;
+      const uint32_t n_next = valid && cj + 1 < rb.nchunk ? __ldg(e + rb.je(cj + 1)) - pi : 0u;
+      const bool next_big = n_next > (uint32_t)kBinWinT;
+      // chunks of <= 32 products ("tiny") are reduced in registers by a shared-memory-free
+      // kernel: windows never mix tiny and other chunks
+      const bool tiny = n <= 32u, next_tiny = n_next <= 32u;
       // ---- reduce windows: runs of small chunks; each sub-bin of a big chunk alone
       // (windows also end every kBinWinT chunks: the direct reducer keeps a cursor per chunk)
       const bool cut = valid && (cj == rb.nchunk - 1 || n > (uint32_t)kBinWinT || next_big || pe / kBinWinT != pi / kBinWinT ||
-                                 ((cj + 1) % kBinWinT) == 0);
+                                 ((cj + 1) % kBinWinT) == 0 || tiny != next_tiny);
       const uint32_t cm = __ballot_sync(0xffffffffu, cut);
       {
         const uint32_t prev = cm & lanemask_lt();
         const int ws = prev ? q0 + 31 - __clz(prev) + 1 : wstart;
         const int wjs = rb.js(ws);
-        emit_items(cut && !big && pi > __ldg(e + wjs), BinItem{(int32_t)h, wjs, je, 0}, wins, nwin);
+        const bool emit = cut && !big && pi > __ldg(e + wjs);
+        emit_items(emit && !tiny, BinItem{(int32_t)h, wjs, je, 0}, wins, nwin);
+        emit_items(emit && tiny, BinItem{(int32_t)h, wjs, je, 0}, wins_t, nwin + 8);
         if (cm) wstart = q0 + 31 - __clz(cm) + 1;
       }
       // big chunks: one item, or column parts of ~kBigSplit elements each (every part
@@ -587,8 +594,9 @@ __device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA 
         __syncwarp();
         if (valid && ((lastm >> lane) & 1u)) wc[ch] = slot + 1;
         if (valid) {
-          rc[slot] = (uint16_t)(cw[u] & cmask);
-          rv[slot] = vw[u];
+          // streaming stores: the reorder buffer must not evict the B rows from L2
+          __stcs(rc + slot, (uint16_t)(cw[u] & cmask));
+          __stcs(rv + slot, vw[u]);
         }
         __syncwarp();
       }
@@ -803,9 +811,10 @@ __device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* sc, const doub
     if (!(s0 <= e0 && e0 <= n)) { printf("sortred r %u s0 %u e0 %u n %u m %u\n", r, s0, e0, n, m); asm volatile("trap;"); }
 #endif
     const uint32_t cl = S.inv[r];
-    c_col[out + r] = colbase + cl;
+    __stcs(c_col + out + r, colbase + cl);
     // association of the column's chunk: bit (cl >> mshift) of seqmask
-    c_val[out + r] = ((seqmask >> (cl >> mshift)) & 1ull) ? sum_seq_s(S.sval, s0, e0) : sum_pairwise_s(S.sval, s0, e0);
+    __stcs(c_val + out + r,
+           ((seqmask >> (cl >> mshift)) & 1ull) ? sum_seq_s(S.sval, s0, e0) : sum_pairwise_s(S.sval, s0, e0));
   }
   __syncwarp();
   return true;
@@ -815,8 +824,7 @@ __device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* sc, const doub
 // lane, sorted by (column, stream position) with a register bitonic network, runs of equal
 // columns summed with the chunk's association -- sequential from +0.0 (dense) or
 // x0 + (((-0.0 + x1) + x2) + ...) (np.add.reduceat, numpy pairwise below 8 terms).
-// Returns 1 ok, 0 count mismatch, -1 when a column has more than 8 products (the caller
-// then takes the general path).
+// Returns 1 ok, 0 count mismatch.
 __device__ __forceinline__ int reduce_chunk_wave(const uint16_t* __restrict__ sc, const double* __restrict__ sv, uint32_t n,
                                                  uint32_t m, bool seq, uint32_t colbase, uint32_t* __restrict__ c_col,
                                                  double* __restrict__ c_val, int64_t out) {
@@ -846,23 +854,107 @@ __device__ __forceinline__ int reduce_chunk_wave(const uint16_t* __restrict__ sc
   const uint32_t after = hm & ~lanemask_le();
   const uint32_t runlen = head ? (after ? (uint32_t)(__ffs(after) - 1) : n) - (uint32_t)lane : 0u;
   const uint32_t maxd = __reduce_max_sync(0xffffffffu, runlen);
-  if (maxd > 8u) return -1;
   double acc = seq ? __dadd_rn(0.0, v) : v;
-  double rest = -0.0;
-  for (uint32_t t = 1; t < maxd; ++t) {
-    const double x = __shfl_sync(0xffffffffu, v, min(lane + (int)t, 31));
-    if (t < runlen) {
-      if (seq) acc = __dadd_rn(acc, x);
-      else rest = __dadd_rn(rest, x);
+  if (maxd <= 8u) {
+    double rest = -0.0;
+    for (uint32_t t = 1; t < maxd; ++t) {
+      const double x = __shfl_sync(0xffffffffu, v, min(lane + (int)t, 31));
+      if (t < runlen) {
+        if (seq) acc = __dadd_rn(acc, x);
+        else rest = __dadd_rn(rest, x);
+      }
+    }
+    if (!seq && runlen > 1) acc = __dadd_rn(acc, rest);
+  } else {
+    // a column with 9..32 products: numpy's pairwise of x1..x_{d-1} (8 strided partial sums,
+    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), the remainder sequentially), streamed over shuffles
+    const int nr = (int)runlen - 1;   // rest terms x_1..x_nr
+    const int full = nr >= 8 ? nr - nr % 8 : 0;
+    double r[8];
+    double res = -0.0;
+    bool combined = nr < 8;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = 0.0;
+#pragma unroll
+    for (int t = 1; t < 32; ++t) {
+      const double x = __shfl_sync(0xffffffffu, v, min(lane + t, 31));
+      if (t <= nr) {
+        if (seq) {
+          acc = __dadd_rn(acc, x);
+        } else if (t - 1 < full) {
+          r[(t - 1) % 8] = t <= 8 ? x : __dadd_rn(r[(t - 1) % 8], x);
+        } else {
+          if (!combined) {
+            res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                            __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+            combined = true;
+          }
+          res = __dadd_rn(res, x);
+        }
+      }
+    }
+    if (!seq && nr > 0) {
+      if (!combined)
+        res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                        __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      acc = __dadd_rn(acc, res);
     }
   }
-  if (!seq && runlen > 1) acc = __dadd_rn(acc, rest);
   const uint32_t rank = __popc(hm & lanemask_lt());
   if (head) {
-    c_col[out + rank] = colbase + c;
-    c_val[out + rank] = acc;
+    __stcs(c_col + out + rank, colbase + c);
+    __stcs(c_val + out + rank, acc);
   }
   return __popc(hm) == m ? 1 : 0;
+}
+
+// Reduce, windows of tiny chunks (<= 32 products each): one warp per window, no shared memory.
+__global__ void __launch_bounds__(256, 4)
+k_bin_reduce_tiny(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, const int64_t* __restrict__ mn,
+                  const int64_t* __restrict__ mx, Sem sem, const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce,
+                  const uint32_t* __restrict__ cd, const int64_t* __restrict__ hbase, int64_t batch_base,
+                  const BinItem* __restrict__ wins, const unsigned long long* __restrict__ nwin,
+                  unsigned long long* __restrict__ ticket, const uint16_t* __restrict__ bcol,
+                  const double* __restrict__ bval, const int64_t* __restrict__ c_rp, uint32_t* __restrict__ c_col,
+                  double* __restrict__ c_val, unsigned long long* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int shift = sem.shift_num, gs = bin_shift_of(shift);
+  const int64_t nw = (int64_t)*nwin;
+  const uint32_t cwmask = ~((1u << shift) - 1u);
+  while (true) {
+    unsigned long long wi = 0;
+    if (lane == 0) wi = atomicAdd(ticket, 1ull);
+    wi = __shfl_sync(0xffffffffu, wi, 0);
+    if ((int64_t)wi >= nw) break;
+    const BinItem it = wins[wi];
+    const int64_t i = rows[it.h];
+    const int ci = cat[i];
+    const RowBins rb = row_bins(mn[i], mx[i], shift);
+    const uint32_t* e = ce + choff[it.h];
+    const uint32_t* d = cd + choff[it.h];
+    const int64_t rowbase = hbase[it.h] - batch_base;
+    const int64_t out_row = c_rp[i];
+    bool ok = true;
+    for (int j0 = it.ja; j0 < it.jb; j0 += 32) {
+      // chunk table entries of 32 chunks (tiny windows: sub-bins == chunks)
+      const uint32_t e_l = j0 + lane <= it.jb ? __ldg(e + j0 + lane) : 0u;
+      const uint32_t d_l = j0 + lane <= it.jb ? __ldg(d + j0 + lane) : 0u;
+      const int jn = min(it.jb - j0, 32);
+      const uint32_t e_last = __ldg(e + j0 + jn), d_last = __ldg(d + j0 + jn);
+      for (int t = 0; t < jn; ++t) {
+        const uint32_t ej = __shfl_sync(0xffffffffu, e_l, t);
+        const uint32_t en = t + 1 < 32 ? __shfl_sync(0xffffffffu, e_l, min(t + 1, 31)) : e_last;
+        const uint32_t dj = __shfl_sync(0xffffffffu, d_l, t);
+        const uint32_t dn = t + 1 < 32 ? __shfl_sync(0xffffffffu, d_l, min(t + 1, 31)) : d_last;
+        const uint32_t n = (t + 1 == jn ? e_last : en) - ej, m = (t + 1 == jn ? d_last : dn) - dj;
+        if (n == 0) continue;
+        const bool seq = ci == kCatDense || (int64_t)n >= sem.crossover;
+        const uint32_t colbase = (uint32_t)((rb.b0 + j0 + t) << gs) & cwmask;
+        ok &= reduce_chunk_wave(bcol + rowbase + ej, bval + rowbase + ej, n, m, seq, colbase, c_col, c_val, out_row + dj) == 1;
+      }
+    }
+    if (!ok && lane == 0) atomicOr(err, 4ull);
+  }
 }
 
 // Reduce: one warp per window.
@@ -919,15 +1011,12 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
       if (n) {
         const bool seq = ci == kCatDense || (int64_t)n >= sem.crossover;
         const uint32_t colbase = (uint32_t)((rb.b0 + j) << gs) & cwmask;
-        int r = -1;
         if (n <= 32u)
-          r = reduce_chunk_wave(bcol + rowbase + ej, bval + rowbase + ej, n, dje - dj, seq, colbase, c_col, c_val,
-                                out_row + dj);
-        if (r < 0)
+          ok &= reduce_chunk_wave(bcol + rowbase + ej, bval + rowbase + ej, n, dje - dj, seq, colbase, c_col, c_val,
+                                  out_row + dj) == 1;
+        else
           ok &= reduce_chunk_sort(bcol + rowbase + ej, bval + rowbase + ej, n, dje - dj, seq ? ~0ull : 0ull, 16,
                                   colbase, S, c_col, c_val, out_row + dj);
-        else
-          ok &= r == 1;
       }
       j = je;
     }
@@ -1201,8 +1290,8 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
       if (lane == 0) atomicAdd(&g_big_stats[5], (unsigned long long)(t_c - t_b));
 #endif
       for (uint32_t r = rlo + lane; r < rhi; r += 32) {
-        c_col[out + r] = colbase + inv[r - rlo];
-        c_val[out + r] = acc[r - rlo];
+        __stcs(c_col + out + r, colbase + (uint32_t)inv[r - rlo]);
+        __stcs(c_val + out + r, acc[r - rlo]);
       }
       __syncwarp();
 #ifdef MG_BIG_STATS

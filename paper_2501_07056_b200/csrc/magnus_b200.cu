@@ -131,6 +131,11 @@ struct magnus_ctx {
   uint32_t* cbm_pool = nullptr;
   uint64_t cbm_cap = 0;
   std::vector<int64_t> h_hinter, h_nent;
+  std::vector<int32_t> h_rows;   // heavy rows, ascending
+  // host readback overlapped with the numeric phase (magnus_numeric_host)
+  uint32_t* host_col = nullptr;
+  double* host_val = nullptr;
+  int64_t host_done = 0;
   int64_t total_ent = 0;
   // direct heavy path (direct_rows.cuh)
   bool direct = false;
@@ -602,6 +607,19 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   ctx->sem.mode_words = (int32_t)((n_chunks_global + 31) / 32);
   // heavy-row workspace
   const int64_t nH = ctx->host_stats[mg::kStatNH];
+  if (nH > 1) {
+    // heavy rows in ascending row order: batches then complete contiguous row ranges (the
+    // host readback overlaps them) and their contents do not depend on atomic order
+    ctx->h_rows.resize(nH);
+    MG_CUDA(cudaMemcpyAsync(ctx->h_rows.data(), ctx->listH, nH * 4, cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    std::sort(ctx->h_rows.begin(), ctx->h_rows.end());
+    MG_CUDA(cudaMemcpyAsync(ctx->listH, ctx->h_rows.data(), nH * 4, cudaMemcpyHostToDevice, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+  } else {
+    ctx->h_rows.assign(nH, 0);
+    if (nH == 1) MG_CUDA(cudaMemcpy(ctx->h_rows.data(), ctx->listH, 4, cudaMemcpyDeviceToHost));
+  }
   MG_CUDA(ctx->alloc(&ctx->modebits, std::max<int64_t>(1, nH) * ctx->sem.mode_words));
   const int64_t maxnk = ctx->host_stats[mg::kStatMaxNk];
   ctx->gk_stride = maxnk > mg::kKSN ? ((maxnk + 8) / 4) * 4 : 4;
@@ -706,9 +724,10 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   }
   const int64_t per_elem = 10;   // u16 local column + f64 product
   int64_t cap = std::min<int64_t>(total, std::min<int64_t>((int64_t)(free_b * 0.2) / per_elem, int64_t(3) << 30));
-#ifdef MG_CAP_ELEMS
-  cap = std::min<int64_t>(cap, MG_CAP_ELEMS);
-#endif
+  if (const char* ce = std::getenv("MAGNUS_BATCH_ELEMS")) {   // testing: force many heavy-row batches
+    const long long v = std::atoll(ce);
+    if (v > 0) cap = std::min<int64_t>(cap, (int64_t)v);
+  }
   cap = std::max(cap, max_row);
   // batches [h0, h1) and the largest chunk-table span of a batch
   std::vector<int64_t> cuts{0};
@@ -742,8 +761,8 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     MG_CUDA(cudaMallocAsync(&bcol[q], (size_t)std::max<int64_t>(buf_elems, 1) * 2 + 64, s));
     MG_CUDA(cudaMallocAsync(&bval[q], (size_t)std::max<int64_t>(buf_elems, 1) * 8 + 64, s));
     // windows and units: <= one per chunk entry; big-chunk parts: <= entries + elements / kBigSplit
-    MG_CUDA(cudaMallocAsync(&items[q], ((size_t)std::max<int64_t>(max_ent, 1) * 2 + (size_t)max_big) * sizeof(mg::BinItem), s));
-    MG_CUDA(cudaMallocAsync(&cnts[q], 64, s));
+    MG_CUDA(cudaMallocAsync(&items[q], ((size_t)std::max<int64_t>(max_ent, 1) * 3 + (size_t)max_big) * sizeof(mg::BinItem), s));
+    MG_CUDA(cudaMallocAsync(&cnts[q], 128, s));
   }
   const size_t big_smem = mg::bin_big_smem(ctx->sem.shift_num);
   int occ_b = 1;
@@ -771,6 +790,13 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
       if (h < nH) a += ctx->h_hinter[h];
     }
   }
+  // host readback: C offset of each batch's end row (the next batch's first heavy row)
+  std::vector<int64_t> batch_end(cuts.size(), -1);
+  if (ctx->host_col) {
+    for (size_t b = 0; b + 2 < cuts.size(); ++b)
+      MG_CUDA(cudaMemcpyAsync(&batch_end[b], c_rp + ctx->h_rows[cuts[b + 1]], 8, cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+  }
   cudaStream_t sr = ctx->aux, sbig = ctx->aux2;
   // the reducers run on the main stream after each batch's expand (measured faster than
   // overlapping them on side streams); MAGNUS_SERIAL=0 restores the concurrent pipeline
@@ -783,6 +809,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     mg::BinItem* wins = static_cast<mg::BinItem*>(items[q]);
     mg::BinItem* units = wins + std::max<int64_t>(max_ent, 1);
     mg::BinItem* bigs = units + std::max<int64_t>(max_ent, 1);
+    mg::BinItem* wins_t = bigs + max_big;   // windows of tiny chunks (k_bin_reduce_tiny)
     auto* nwin = static_cast<unsigned long long*>(cnts[q]);
     auto* nunit = nwin + 1;
     auto* nbig = nwin + 2;
@@ -791,10 +818,10 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
       MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_b[q], 0));
     }
     used[q] = true;
-    MG_CUDA(cudaMemsetAsync(cnts[q], 0, 64, s));
+    MG_CUDA(cudaMemsetAsync(cnts[q], 0, 128, s));
     ctx->begin(MAGNUS_K_BIN_PLAN);
     mg::k_bin_plan<<<(unsigned)std::min<int64_t>((h1 - h0 + 7) / 8, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
-        ctx->listH, h0, h1, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, wins, nwin, bigs, nbig, units,
+        ctx->listH, h0, h1, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, wins, nwin, wins_t, bigs, nbig, units,
         nunit, std::max<int64_t>(max_ent, 1), max_big);
     ctx->end();
     ctx->begin(MAGNUS_K_BIN_EXPAND);
@@ -828,8 +855,27 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
         ctx->listH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->hbase, hb[b], wins, nwin,
         nwin + 4, static_cast<const uint16_t*>(bcol[q]), static_cast<const double*>(bval[q]), c_rp, c_col, c_val, ctx->err);
     ctx->end_on(MAGNUS_K_BIN_REDUCE, m2, sr);
+    cudaEvent_t m3 = ctx->begin_on(MAGNUS_K_BIN_REDUCE, sr);
+    mg::k_bin_reduce_tiny<<<(unsigned)(ctx->sm_count * 8), 256, 0, sr>>>(
+        ctx->listH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->hbase, hb[b], wins_t, nwin + 8,
+        nwin + 9, static_cast<const uint16_t*>(bcol[q]), static_cast<const double*>(bval[q]), c_rp, c_col, c_val, ctx->err);
+    ctx->end_on(MAGNUS_K_BIN_REDUCE, m3, sr);
     MG_CUDA(cudaEventRecord(ctx->ev_r[q], sr));
     MG_CUDA(cudaGetLastError());
+    if (ctx->host_col && sr == s && sbig == s) {
+      // rows below the next batch's first heavy row are complete (light rows ran first):
+      // read that prefix of C back on the copy stream while the next batch computes
+      const int64_t end = b + 2 < cuts.size() ? batch_end[b] : -1;
+      if (end > ctx->host_done) {
+        MG_CUDA(cudaEventRecord(ctx->ev_fork, s));
+        MG_CUDA(cudaStreamWaitEvent(ctx->aux3, ctx->ev_fork, 0));
+        MG_CUDA(cudaMemcpyAsync(ctx->host_col + ctx->host_done, c_col + ctx->host_done, (end - ctx->host_done) * 4,
+                                cudaMemcpyDeviceToHost, ctx->aux3));
+        MG_CUDA(cudaMemcpyAsync(ctx->host_val + ctx->host_done, c_val + ctx->host_done, (end - ctx->host_done) * 8,
+                                cudaMemcpyDeviceToHost, ctx->aux3));
+        ctx->host_done = end;
+      }
+    }
   }
   for (int q = 0; q < nbuf; ++q) {
     if (!used[q]) continue;
@@ -1013,6 +1059,33 @@ int magnus_debug_big_stats(unsigned long long* out8) {
 #else
   for (int i = 0; i < 8; ++i) out8[i] = 0;
 #endif
+  return MAGNUS_OK;
+}
+
+int magnus_numeric_host(magnus_ctx* ctx, const int64_t* c_row_ptr, uint32_t* c_col, double* c_val, uint32_t* c_col_host,
+                        double* c_val_host, magnus_counters* counters, void* stream) {
+  if (!ctx || !c_col_host || !c_val_host) return set_err(MAGNUS_INPUT, "null argument");
+  ctx->host_col = c_col_host;
+  ctx->host_val = c_val_host;
+  ctx->host_done = 0;
+  int rc = magnus_numeric(ctx, c_row_ptr, c_col, c_val, counters, stream);
+  const int64_t done = ctx->host_done;
+  ctx->host_col = nullptr;
+  ctx->host_val = nullptr;
+  if (rc) {
+    cudaStreamSynchronize(ctx->aux3);
+    return rc;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t nnz = 0;
+  if (ctx->A.n_rows > 0) MG_CUDA(cudaMemcpyAsync(&nnz, c_row_ptr + ctx->A.n_rows, 8, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  if (nnz > done) {
+    MG_CUDA(cudaMemcpyAsync(c_col_host + done, c_col + done, (nnz - done) * 4, cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaMemcpyAsync(c_val_host + done, c_val + done, (nnz - done) * 8, cudaMemcpyDeviceToHost, s));
+  }
+  MG_CUDA(cudaStreamSynchronize(ctx->aux3));
+  MG_CUDA(cudaStreamSynchronize(s));
   return MAGNUS_OK;
 }
 

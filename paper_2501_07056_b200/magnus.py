@@ -156,8 +156,10 @@ class MagnusPlan:
         self.row_ptr, self.nnz = rp, int(nnz.value)
         return rp
 
-    def numeric(self, row_ptr=None, out=None):
-        """magnus_numeric (reference magnus.py:459-542): fills C; returns (C, counters)."""
+    def numeric(self, row_ptr=None, out=None, host_out=None):
+        """magnus_numeric (reference magnus.py:459-542): fills C; returns (C, counters).
+        host_out=(col, val): host tensors (page-locked for overlap) that receive C's col / val;
+        completed row ranges are read back while later row batches compute."""
         torch = _torch()
         rp = self.row_ptr if row_ptr is None else row_ptr
         if rp is None or rp is not self.row_ptr:
@@ -168,9 +170,18 @@ class MagnusPlan:
         else:
             col, val = out
         cnt = _lib.Counters()
-        _lib.check(_lib.lib().magnus_numeric(self.ctx.h, C.c_void_p(rp.data_ptr()), C.c_void_p(col.data_ptr()),
-                                             C.c_void_p(val.data_ptr()), C.byref(cnt),
-                                             C.c_void_p(self.stream.cuda_stream)))
+        if host_out is None:
+            _lib.check(_lib.lib().magnus_numeric(self.ctx.h, C.c_void_p(rp.data_ptr()), C.c_void_p(col.data_ptr()),
+                                                 C.c_void_p(val.data_ptr()), C.byref(cnt),
+                                                 C.c_void_p(self.stream.cuda_stream)))
+        else:
+            hc, hv = host_out
+            if hc.numel() < self.nnz or hv.numel() < self.nnz or hc.is_cuda or hv.is_cuda:
+                raise InputError("host_out buffers must be host tensors with at least nnz(C) entries")
+            _lib.check(_lib.lib().magnus_numeric_host(self.ctx.h, C.c_void_p(rp.data_ptr()), C.c_void_p(col.data_ptr()),
+                                                      C.c_void_p(val.data_ptr()), C.c_void_p(hc.data_ptr()),
+                                                      C.c_void_p(hv.data_ptr()), C.byref(cnt),
+                                                      C.c_void_p(self.stream.cuda_stream)))
         counters = {n: int(getattr(cnt, n)) for n, _ in _lib.Counters._fields_}
         return CsrMatrix(self.A.n_rows, self.B.n_cols, rp, col, val, canonical=True), counters
 

@@ -203,3 +203,28 @@ def test_direct_heavy_path(case, sysname, monkeypatch):
     sysp = {"b200": B200, "fine4k": FINE4K}[sysname]
     ref = oracle.spgemm(A, B, sysp)
     assert_same(spgemm_magnus(A, B, sys=sysp), ref)
+
+
+@pytest.mark.parametrize("batch_elems", [0, 20000])
+def test_numeric_host_readback(batch_elems, monkeypatch):
+    """magnus_numeric_host: C read back into host buffers (overlapped with later heavy-row
+    batches; MAGNUS_BATCH_ELEMS forces many batches) equals C on the device, and the
+    heavy-row batches (in row order) give the oracle's bits."""
+    from paper_2501_07056_b200 import MagnusPlan
+    if batch_elems:
+        monkeypatch.setenv("MAGNUS_BATCH_ELEMS", str(batch_elems))
+    A = generate.rmat(14, 16, seed=31)
+    dev = torch.device("cuda")
+    Ad = CsrMatrix(A.n_rows, A.n_cols, torch.from_numpy(A.row_ptr).to(dev), torch.from_numpy(A.col).to(dev),
+                   torch.from_numpy(A.val).to(dev))
+    plan = MagnusPlan(Ad, Ad, sys=B200)
+    rp = plan.symbolic()
+    hc = torch.empty(plan.nnz, dtype=torch.int32).pin_memory()
+    hv = torch.empty(plan.nnz, dtype=torch.float64).pin_memory()
+    C, _ = plan.numeric(rp, host_out=(hc, hv))
+    plan.close()
+    assert torch.equal(hc, C.col.cpu()) and torch.equal(hv.view(torch.int64), C.val.cpu().view(torch.int64))
+    ref = oracle.spgemm(A, A, B200)
+    np.testing.assert_array_equal(rp.cpu().numpy(), ref.row_ptr)
+    np.testing.assert_array_equal(hc.numpy().view(np.uint32), ref.col)
+    np.testing.assert_array_equal(hv.numpy().view(np.uint64), ref.val.view(np.uint64))
