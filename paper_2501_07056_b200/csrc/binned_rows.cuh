@@ -1040,7 +1040,7 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
 // bytes per warp are in flight without registers.  Chunks above kBigSplit
 // elements are split into column parts handled by different warps.
 #ifndef MG_BIG_D
-#define MG_BIG_D 2048
+#define MG_BIG_D 1024
 #endif
 constexpr int kBigD = MG_BIG_D;            // ranks accumulated per pass
 #ifndef MG_BIG_RS
@@ -1051,7 +1051,10 @@ constexpr int kBigRunSer = MG_BIG_RS;      // waves with fewer run breaks are ap
 #define MG_BIG_NS 2
 #endif
 constexpr int kBigNS = MG_BIG_NS;          // ring stages per warp
-constexpr int kBigSE = 256;                // elements per stage
+#ifndef MG_BIG_SE
+#define MG_BIG_SE 128
+#endif
+constexpr int kBigSE = MG_BIG_SE;          // elements per stage
 constexpr int kBigSC = kBigSE * 2 + 16;    // stage bytes: columns (+ alignment slack)
 constexpr int kBigSV = kBigSE * 8 + 16;    // stage bytes: values (+ alignment slack)
 #ifdef MG_BIG_STATS
