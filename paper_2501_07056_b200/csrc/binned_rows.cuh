@@ -38,7 +38,10 @@
 namespace mg {
 
 constexpr int kBinT = 128;            // threads per CTA of the expand / reduce kernels (4 warps)
-constexpr int kBinE = 512;            // small chunk: <= kBinE elements (sort path); packed windows < kBinE
+#ifndef MG_BIN_E
+#define MG_BIN_E 512
+#endif
+constexpr int kBinE = MG_BIN_E;       // small chunk: <= kBinE elements (sort path); packed windows < kBinE
 constexpr int kBinWinT = kBinE / 2;   // window packing quantum
 constexpr int kBinMaxShift = 14;      // chunk width <= 16384 columns (u16 chunk-local columns)
 constexpr int kSubShift = 14;         // table granularity (sub-bin == chunk while shift_num <= 14)
