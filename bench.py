@@ -329,6 +329,11 @@ def main():
         nnz_c = int(t)
     comp = compulsory_bytes(A.n_rows, A.col.numel(), total_inter, nnz_c, A.row_ptr.element_size(),
                             B.row_ptr.element_size(), 8, A.n_rows)
+    # the paper's two-pass minimum-data-volume model (reference bound.py:44-72), for comparability
+    from paper_2501_07056_b200 import bound_inputs_for, ideal_bound
+    ib_r, ib_w, ib_t = ideal_bound(bound_inputs_for(A, B, nnz_c, total_inter, peak * 1e9 * world))
+    ideal = {"read_bytes": int(ib_r), "write_bytes": int(ib_w), "t_ideal_ms": round(ib_t * 1e3, 3),
+             "multiple": round(ms_step / (ib_t * 1e3), 2), "bandwidth": "measured HBM peak x n_gpus"}
 
     # e2e: host buffers through the public API (H2D of A, B + D2H of C inside the timed region)
     e2e = None
@@ -369,6 +374,7 @@ def main():
                          "traffic_source": "profiles/r1_cfg3_traffic.json (ncu dram__bytes_read+write, mean per launch)"
                          if traffic else None,
                          "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4)},
+            "ideal_bound": ideal,
             "kernel_ms": prof_share,
             "heavy_chunks": hs,
             "e2e": e2e,

@@ -4,12 +4,14 @@ reference package's `spgemm_magnus` (arxiv/paper_2501_07056, magnus.py:545-583).
 Public API (same names as the reference):
     spgemm_magnus, CsrMatrix, RowStats, SystemParams, ChunkPlan, compute_chunk_plan,
     with_overrides, AccumThresholds, select_accumulator, merge_chunks_for_sort,
-    SpgemmResult, RowCategories, row_intermediate_stats and the error classes.
+    SpgemmResult, RowCategories, row_intermediate_stats, IdealBoundInputs / ideal_bound /
+    bound_inputs_for (the paper's minimum-data-volume model) and the error classes.
 Device-only additions: detect_device_params, MagnusPlan (the two phases),
 parallel.spgemm_magnus_distributed (row-block split over ranks).
 """
 
 from .accumulators import Accum, AccumThresholds, merge_chunks_for_sort, select_accumulator
+from .bound import IdealBoundInputs, bound_inputs_for, col_index_bytes, ideal_bound
 from .errors import ContractViolation, InputError, OverBudgetError, ParseError, SpgemmError
 from .matrix import CsrMatrix, RowStats, validate_csr
 from .planner import (NUMERIC, SYMBOLIC, ChunkPlan, SystemParams, b200_default_params, compute_chunk_plan,
@@ -19,7 +21,8 @@ __all__ = [
     "Accum", "AccumThresholds", "merge_chunks_for_sort", "select_accumulator", "ContractViolation", "InputError",
     "OverBudgetError", "ParseError", "SpgemmError", "CsrMatrix", "RowStats", "validate_csr", "NUMERIC", "SYMBOLIC",
     "ChunkPlan", "SystemParams", "b200_default_params", "compute_chunk_plan", "detect_device_params", "with_overrides",
-    "spgemm_magnus", "SpgemmResult", "RowCategories", "MagnusPlan", "row_intermediate_stats",
+    "spgemm_magnus", "SpgemmResult", "RowCategories", "MagnusPlan", "row_intermediate_stats", "IdealBoundInputs",
+    "bound_inputs_for", "col_index_bytes", "ideal_bound",
 ]
 
 

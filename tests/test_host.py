@@ -126,3 +126,23 @@ def test_generators_are_deterministic_and_canonical():
     s = generate.stencil27(8)
     validate_csr(s)
     assert s.nnz == (3 * 8 - 2) ** 3
+
+
+def test_ideal_bound_formula():
+    """reference bound.py:44-53: two-pass read volume and single write of C."""
+    from paper_2501_07056_b200 import IdealBoundInputs, InputError, bound_inputs_for, col_index_bytes, ideal_bound
+    inp = IdealBoundInputs(n_a=10, nnz_a=30, n_inter_prod=100, n_c=10, nnz_c=50, s_row_ptr=8, s_col_idx=4, s_val=8,
+                           bandwidth_bytes_per_sec=1e3)
+    r, w, t = ideal_bound(inp)
+    assert r == 2 * 11 * 8 + 30 * (32 + 8 + 8) + 100 * (8 + 8)
+    assert w == 11 * 8 + 50 * 12
+    assert t == (r + w) / 1e3
+    assert col_index_bytes(2 ** 32) == 4 and col_index_bytes(2 ** 32 + 1) == 8
+    with pytest.raises(InputError):
+        IdealBoundInputs(n_a=-1, nnz_a=0, n_inter_prod=0, n_c=0, nnz_c=0)
+    with pytest.raises(InputError):
+        IdealBoundInputs(n_a=1, nnz_a=0, n_inter_prod=0, n_c=0, nnz_c=0, bandwidth_bytes_per_sec=0)
+    from paper_2501_07056_b200 import generate
+    A = generate.uniform_rows(64, 64, 4, seed=1)
+    b = bound_inputs_for(A, A, nnz_c=200, n_inter_prod=256, bandwidth_bytes_per_sec=2.0)
+    assert (b.n_a, b.nnz_a, b.s_row_ptr, b.s_col_idx, b.s_val) == (64, 256, 8, 4, 8)
