@@ -337,8 +337,19 @@ def main():
 
     # e2e: host buffers through the public API (H2D of A, B + D2H of C inside the timed region)
     e2e = None
-    if not args.no_e2e and rank == 0 and world == 1:
-        e2e = run_e2e(A, B, sysp, args.e2e_steps or max(1, min(args.steps, 3)), total_inter)
+    if not args.no_e2e:
+        # every rank: its row block of A and all of B from host memory, its C block back to host
+        e2e = run_e2e(A_loc, B, sysp, args.e2e_steps or max(1, min(args.steps, 3)), total_inter)
+        if world > 1:
+            t = torch.tensor([e2e["ms_per_step"], e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"]],
+                             dtype=torch.float64, device=device)
+            tmax = t.clone()
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t)
+            ms = float(tmax[0])
+            e2e = {"value": round(2.0 * total_inter / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+                   "h2d_bytes_per_step": int(t[1]), "d2h_bytes_per_step": int(t[2]), "ms_per_step": round(ms, 2),
+                   "steps": e2e["steps"], "timing": "max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
