@@ -140,6 +140,7 @@ struct magnus_ctx {
   // direct heavy path (direct_rows.cuh)
   bool direct = false;
   bool sym2 = false;   // heavy symbolic: k_heavy_sym2 (symbolic_rows.cuh)
+  int sym2_occ = 1;
   int dir_wlog = 0;
   int dir_occ = 1;
   int64_t dir_nwin1 = 0, dir_min_len = 0, dir_nidx = 0, kst_stride = 0;
@@ -331,6 +332,8 @@ int magnus_ctx_create(magnus_ctx** out) {
                                (int)mg::Exp2Smem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_heavy_sym2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::Sym2Smem::kTotal));
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->sym2_occ, mg::k_heavy_sym2, mg::kS2T, mg::Sym2Smem::kTotal));
+  c->sym2_occ = std::max(1, std::min(c->sym2_occ, 7));
   MG_CUDA(cudaFuncSetAttribute(mg::k_dir_num, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)(mg::DirSmem::kWarp * mg::kDirNW)));
 
@@ -924,7 +927,8 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
           ctx->A, ctx->B, ctx->listH, nH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->modebits, c_rp, c_col, c_val, ctx->gk,
           ctx->gk_stride, ctx->work, ctx->err);
     else if (ctx->binned && ctx->sym2)
-      mg::k_heavy_sym2<<<(unsigned)std::min<int64_t>(nH, ctx->sm_count), mg::kS2T, mg::Sym2Smem::kTotal, s>>>(
+      mg::k_heavy_sym2<<<(unsigned)std::min<int64_t>(nH, (int64_t)ctx->sm_count * ctx->sym2_occ), mg::kS2T,
+                         mg::Sym2Smem::kTotal, s>>>(
           ctx->A, ctx->B, ctx->listH, nH, ctx->mn, ctx->mx, (int)ctx->sem.shift_num, ctx->counts, ctx->choff, ctx->ce,
           ctx->cd, ctx->cbm_pool, ctx->cbm_slot, ctx->cbm_cap, ctx->work, ctx->bslot, ctx->bidx, ctx->dir_nwin1,
           ctx->dir_wlog, ctx->gk, ctx->gk_stride);

@@ -20,12 +20,24 @@
 
 namespace mg {
 
-constexpr int kS2T = 1024;                 // threads per CTA (1 CTA / SM)
-constexpr int kS2WinLog = 20;              // bitmap window: 2^20 columns (128 KB)
+#ifndef MG_S2_T
+#define MG_S2_T 1024
+#endif
+#ifndef MG_S2_WIN
+#define MG_S2_WIN 20
+#endif
+#ifndef MG_S2_TOUCH
+#define MG_S2_TOUCH 8192
+#endif
+#ifndef MG_S2_K
+#define MG_S2_K 4096
+#endif
+constexpr int kS2T = MG_S2_T;              // threads per CTA
+constexpr int kS2WinLog = MG_S2_WIN;       // bitmap window: 2^20 columns (128 KB)
 constexpr int kS2Words = (1 << kS2WinLog) / 32;
-constexpr int kS2Touch = 8192;             // touched-word list (full scan of the row's words beyond it)
+constexpr int kS2Touch = MG_S2_TOUCH;             // touched-word list (full scan of the row's words beyond it)
 constexpr int kS2Chunks = 2048;            // chunk counters per row
-constexpr int kS2K = 4096;                 // k's whose stream offsets live in shared memory
+constexpr int kS2K = MG_S2_K;                 // k's whose stream offsets live in shared memory
 constexpr int kS2U = 4;                    // waves of loads in flight per warp
 
 struct Sym2Smem {
@@ -35,7 +47,7 @@ struct Sym2Smem {
   static constexpr size_t kK = (size_t)(kS2K + 32) * 4 * 2;
   static constexpr size_t kScratch = 64 * 8;
   static constexpr size_t kTotal = kBitmap + kTouch + kCnt + kK + kScratch;
-  static_assert(kTotal <= 232448 - 1024, "one CTA per SM");
+  static_assert(kTotal <= 232448 - 1024, "fits one SM");
 };
 
 // segment [p0, p1) of B row k inside columns [lo, hi) (hi_all: no upper bound)
@@ -143,7 +155,7 @@ __device__ __forceinline__ void sym2_stream(const DevCsr& B, KP koff, KP kpos, i
   }
 }
 
-__global__ void __launch_bounds__(kS2T, 1)
+__global__ void __launch_bounds__(kS2T)
 k_heavy_sym2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __restrict__ mn,
              const int64_t* __restrict__ mx, int shift, int64_t* __restrict__ counts, const int64_t* __restrict__ choff,
              uint32_t* __restrict__ ce, uint32_t* __restrict__ cd, uint32_t* __restrict__ cbm_pool,
