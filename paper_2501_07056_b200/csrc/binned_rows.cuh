@@ -911,6 +911,18 @@ __device__ __forceinline__ int reduce_chunk_wave(const uint16_t* __restrict__ sc
   return __popc(hm) == m ? 1 : 0;
 }
 
+// Prefetch the reorder-buffer range [q0, q1) of a window (columns + values) into L2: the
+// window's chunks are then reduced from L2 instead of one DRAM round trip each.
+__device__ __forceinline__ void prefetch_slice(const uint16_t* bcol, const double* bval, int64_t q0, int64_t q1) {
+  const int lane = threadIdx.x & 31;
+  const char* c0 = reinterpret_cast<const char*>(bcol + q0);
+  const char* c1 = reinterpret_cast<const char*>(bcol + q1);
+  for (const char* p = c0 + lane * 128; p < c1; p += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  const char* v0 = reinterpret_cast<const char*>(bval + q0);
+  const char* v1 = reinterpret_cast<const char*>(bval + q1);
+  for (const char* p = v0 + lane * 128; p < v1; p += 32 * 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // Reduce, windows of tiny chunks (<= 32 products each): one warp per window, no shared memory.
 __global__ void __launch_bounds__(256, 4)
 k_bin_reduce_tiny(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, const int64_t* __restrict__ mn,
@@ -937,6 +949,7 @@ k_bin_reduce_tiny(const int32_t* __restrict__ rows, const int8_t* __restrict__ c
     const uint32_t* d = cd + choff[it.h];
     const int64_t rowbase = hbase[it.h] - batch_base;
     const int64_t out_row = c_rp[i];
+    prefetch_slice(bcol, bval, rowbase + __ldg(e + it.ja), rowbase + __ldg(e + it.jb));
     bool ok = true;
     for (int j0 = it.ja; j0 < it.jb; j0 += 32) {
       // chunk table entries of 32 chunks (tiny windows: sub-bins == chunks)
@@ -997,6 +1010,7 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
     const uint32_t* d = cd + choff[it.h];
     const int64_t rowbase = hbase[it.h] - batch_base;
     const int64_t out_row = c_rp[i];
+    prefetch_slice(bcol, bval, rowbase + __ldg(e + it.ja), rowbase + __ldg(e + it.jb));
     bool ok = true;
     // chunk table entries of the window, 32 chunks per load (lane l: chunk j0 + l)
     int j0 = -1 << 30;
@@ -1159,6 +1173,30 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
 #ifdef MG_BIG_STATS
     long long t_a = clock64();
 #endif
+    const uint32_t nst = (n + kBigSE - 1) / kBigSE;   // stages of one pass over the slice
+    // stage j of the slice -> ring slot; copies of 16-byte aligned supersets
+    auto issue = [&](uint32_t j) {
+      const uint32_t slot = uses % kBigNS;
+      ++uses;
+      if (lane == 0) {
+        const uint32_t q0 = j * kBigSE, cnt = min((uint32_t)kBigSE, n - q0);
+        const uintptr_t ca = reinterpret_cast<uintptr_t>(sc + q0), va = reinterpret_cast<uintptr_t>(sv + q0);
+        const uintptr_t ca0 = ca & ~uintptr_t(15), va0 = va & ~uintptr_t(15);
+        const uint32_t cb = (uint32_t)(((ca + cnt * 2 - ca0) + 15) & ~uintptr_t(15));
+        const uint32_t vb = (uint32_t)(((va + cnt * 8 - va0) + 15) & ~uintptr_t(15));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        bulk_load2(bars + slot, stc0 + (size_t)slot * kBigSC, reinterpret_cast<const void*>(ca0), cb,
+                   stv0 + (size_t)slot * kBigSV, reinterpret_cast<const void*>(va0), vb);
+      }
+    };
+    // the first stages of the first pass do not depend on the column bitmap: issue them now
+    const uint32_t u_first = uses;
+    const uint32_t n_first = min(nst, (uint32_t)kBigNS);
+    for (uint32_t j = 0; j < n_first; ++j) issue(j);
+    auto drain_first = [&]() {   // consume the early stages when no pass runs
+      for (uint32_t j = 0; j < n_first; ++j) mbar_wait(bars + (u_first + j) % kBigNS, ((u_first + j) / kBigNS) & 1u);
+      __syncwarp();
+    };
     // ---- columns of the chunk -> ranks (bitmap kept by the symbolic pass, else marked here)
     const uint32_t bslot = cbm_slot != nullptr ? __ldg(cbm_slot + choff[it.h] + it.ja) : 0xffffffffu;
     if (bslot != 0xffffffffu) {
@@ -1184,6 +1222,7 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
       if (lane == 0) printf("bin_big mismatch row %lld h %d ja %d jb %d n %u m %u bslot %u\n", (long long)i, it.h, it.ja, it.jb, n, m, bslot);
 #endif
       if (lane == 0) atomicOr(err, 4ull);
+      drain_first();
       continue;
     }
 #ifdef MG_BIG_STATS
@@ -1192,28 +1231,16 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
 #endif
     const uint32_t rlo0 = plo < width ? rank_of(bm, pref, plo) : m;
     const uint32_t rhi0 = phi < width ? rank_of(bm, pref, phi) : m;
-    const uint32_t nst = (n + kBigSE - 1) / kBigSE;   // stages of one pass over the slice
-    // stage j of the slice -> ring slot; copies of 16-byte aligned supersets
-    auto issue = [&](uint32_t j) {
-      const uint32_t slot = uses % kBigNS;
-      ++uses;
-      if (lane == 0) {
-        const uint32_t q0 = j * kBigSE, cnt = min((uint32_t)kBigSE, n - q0);
-        const uintptr_t ca = reinterpret_cast<uintptr_t>(sc + q0), va = reinterpret_cast<uintptr_t>(sv + q0);
-        const uintptr_t ca0 = ca & ~uintptr_t(15), va0 = va & ~uintptr_t(15);
-        const uint32_t cb = (uint32_t)(((ca + cnt * 2 - ca0) + 15) & ~uintptr_t(15));
-        const uint32_t vb = (uint32_t)(((va + cnt * 8 - va0) + 15) & ~uintptr_t(15));
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        bulk_load2(bars + slot, stc0 + (size_t)slot * kBigSC, reinterpret_cast<const void*>(ca0), cb,
-                   stv0 + (size_t)slot * kBigSV, reinterpret_cast<const void*>(va0), vb);
-      }
-    };
     // ---- sums, kBigD ranks per pass
+    if (rlo0 >= rhi0) drain_first();
     for (uint32_t rlo = rlo0; rlo < rhi0; rlo += kBigD) {
       const uint32_t rhi = min(rhi0, rlo + kBigD);
       for (uint32_t r = lane; r < rhi - rlo; r += 32) acc[r] = 0.0;
-      const uint32_t u0 = uses;   // ring use index of stage 0 of this pass
-      for (uint32_t j = 0; j < min(nst, (uint32_t)kBigNS); ++j) issue(j);
+      uint32_t u0 = u_first;   // ring use index of stage 0 of this pass
+      if (rlo != rlo0) {
+        u0 = uses;
+        for (uint32_t j = 0; j < min(nst, (uint32_t)kBigNS); ++j) issue(j);
+      }
       __syncwarp();
       for (uint32_t j = 0; j < nst; ++j) {
         const uint32_t use = u0 + j, slot = use % kBigNS;
