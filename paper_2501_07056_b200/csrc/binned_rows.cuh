@@ -67,6 +67,18 @@ constexpr int kBigMaxParts = 32;
 
 __host__ __device__ inline int bin_shift_of(int shift_num) { return shift_num < kSubShift ? shift_num : kSubShift; }
 
+// A big chunk (or one column part of it), resolved by the plan kernel so that the reducer
+// needs one load per item: its slice in the reorder buffer, its place in C, its bitmap slot.
+struct BigItem {
+  int64_t slice;     // first element in the reorder buffer (batch-relative)
+  int64_t out;       // first C entry of the chunk
+  uint32_t n, m;     // products, distinct columns
+  uint32_t colbase;  // first column of the chunk
+  uint32_t bslot;    // column-bitmap slot in the pool (0xffffffff: none)
+  uint32_t kind;     // column part (kind & 0xffff) of (kind >> 16) parts
+  uint32_t pad;
+};
+
 struct BinItem {   // table entries (sub-bins) [ja, jb) of heavy row h
   int32_t h, ja, jb, kind;   // unit: 1 = whole row; big chunk: column part (kind & 0xffff) of (kind >> 16) parts
 };
@@ -166,8 +178,10 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
                            const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff,
                            const uint32_t* __restrict__ ce, BinItem* __restrict__ wins, unsigned long long* __restrict__ nwin,
                            BinItem* __restrict__ wins_t,
-                           BinItem* __restrict__ bigs, unsigned long long* __restrict__ nbig, BinItem* __restrict__ units,
-                           unsigned long long* __restrict__ nunit, int64_t cap_units, int64_t cap_bigs) {
+                           BigItem* __restrict__ bigs, unsigned long long* __restrict__ nbig, BinItem* __restrict__ units,
+                           unsigned long long* __restrict__ nunit, int64_t cap_units, int64_t cap_bigs,
+                           const uint32_t* __restrict__ cd, const int64_t* __restrict__ hbase, int64_t batch_base,
+                           const int64_t* __restrict__ c_rp, const uint32_t* __restrict__ cbm_slot) {
   const int lane = threadIdx.x & 31;
   unsigned long long* nunit_back = nwin + 6;
   unsigned long long* nbig_back = nwin + 7;
@@ -213,8 +227,19 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
         const int parts = (int)min((uint32_t)kBigMaxParts, (n + kBigSplit - 1) / kBigSplit);
         const bool large = n >= kBigFront;
         const unsigned long long b0i = atomicAdd(large ? nbig : nbig_back, (unsigned long long)parts);
-        for (int pp = 0; pp < parts; ++pp)
-          bigs[large ? (int64_t)(b0i + pp) : cap_bigs - 1 - (int64_t)(b0i + pp)] = BinItem{(int32_t)h, js, je, (parts << 16) | pp};
+        const uint32_t* d = cd + choff[h];
+        BigItem bi;
+        bi.slice = hbase[h] - batch_base + pe;
+        bi.out = c_rp[i] + __ldg(d + js);
+        bi.n = n;
+        bi.m = __ldg(d + je) - __ldg(d + js);
+        bi.colbase = (uint32_t)(((rb.b0 + js) >> rb.cs) << shift);
+        bi.bslot = cbm_slot != nullptr ? __ldg(cbm_slot + choff[h] + js) : 0xffffffffu;
+        bi.pad = 0;
+        for (int pp = 0; pp < parts; ++pp) {
+          bi.kind = ((uint32_t)parts << 16) | (uint32_t)pp;
+          bigs[large ? (int64_t)(b0i + pp) : cap_bigs - 1 - (int64_t)(b0i + pp)] = bi;
+        }
       }
       // ---- expand units: chunk ranges (whole chunks, so small-chunk slices stay in one unit)
       const bool ucut = valid && (cj == rb.nchunk - 1 ||
@@ -1124,12 +1149,9 @@ struct BigStage {
 };
 
 __global__ void __launch_bounds__(32)
-k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, const int64_t* __restrict__ mx, Sem sem,
-          const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce, const uint32_t* __restrict__ cd,
-          const int64_t* __restrict__ hbase, int64_t batch_base, const BinItem* __restrict__ bigs,
-          const unsigned long long* __restrict__ nbig, unsigned long long* __restrict__ ticket, int64_t cap_bigs,
-          const uint32_t* __restrict__ cbm_pool, const uint32_t* __restrict__ cbm_slot,
-          const uint16_t* __restrict__ bcol, const double* __restrict__ bval, const int64_t* __restrict__ c_rp,
+k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* __restrict__ nbig,
+          unsigned long long* __restrict__ ticket, int64_t cap_bigs,
+          const uint32_t* __restrict__ cbm_pool, const uint16_t* __restrict__ bcol, const double* __restrict__ bval,
           uint32_t* __restrict__ c_col, double* __restrict__ c_val, unsigned long long* __restrict__ err) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int shift = sem.shift_num;
@@ -1151,23 +1173,20 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
   __syncwarp();
   uint32_t uses = 0;   // stage fills issued so far (ring position and parity)
   const uint64_t nb_front = nbig[0], nbg = nb_front + nbig[5];   // nbig[5] = back counter (cnts[7])
+  // items by dynamic tickets (large-first list); the next ticket is taken while the current
+  // item is reduced
+  unsigned long long t_next = 0;
+  if (lane == 0) t_next = atomicAdd(ticket, 1ull);
   while (true) {
-    unsigned long long bi = 0;
-    if (lane == 0) bi = atomicAdd(ticket, 1ull);
-    bi = __shfl_sync(0xffffffffu, bi, 0);
-    if (bi >= nbg) break;
-    const BinItem it = bigs[list_slot(bi, nb_front, cap_bigs)];
-    const int64_t i = rows[it.h];
-    const RowBins rb = row_bins(mn[i], mx[i], shift);
-    const uint32_t* e = ce + choff[it.h];
-    const uint32_t* d = cd + choff[it.h];
-    const uint32_t ej = __ldg(e + it.ja), n = __ldg(e + it.jb) - ej;
-    const uint32_t dj = __ldg(d + it.ja), m = __ldg(d + it.jb) - dj;
-    const int64_t rowbase = hbase[it.h] - batch_base;
-    const uint16_t* sc = bcol + rowbase + ej;
-    const double* sv = bval + rowbase + ej;
-    const int64_t out = c_rp[i] + dj;
-    const uint32_t colbase = (uint32_t)(((rb.b0 + it.ja) >> rb.cs) << shift);
+    const uint64_t t = __shfl_sync(0xffffffffu, t_next, 0);
+    if (t >= nbg) break;
+    const BigItem it = bigs[list_slot(t, nb_front, cap_bigs)];
+    if (lane == 0) t_next = atomicAdd(ticket, 1ull);
+    const uint32_t n = it.n, m = it.m;
+    const uint16_t* sc = bcol + it.slice;
+    const double* sv = bval + it.slice;
+    const int64_t out = it.out;
+    const uint32_t colbase = it.colbase;
     const uint32_t parts = (uint32_t)it.kind >> 16, part = (uint32_t)it.kind & 0xffffu;
     const uint32_t plo = (uint32_t)(((uint64_t)width * part) / parts), phi = (uint32_t)(((uint64_t)width * (part + 1)) / parts);
 #ifdef MG_BIG_STATS
@@ -1198,7 +1217,7 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
       __syncwarp();
     };
     // ---- columns of the chunk -> ranks (bitmap kept by the symbolic pass, else marked here)
-    const uint32_t bslot = cbm_slot != nullptr ? __ldg(cbm_slot + choff[it.h] + it.ja) : 0xffffffffu;
+    const uint32_t bslot = it.bslot;
     if (bslot != 0xffffffffu) {
       for (int wd = lane; wd < nwords; wd += 32) bm[wd] = __ldg(cbm_pool + (size_t)bslot * nwords + wd);
     } else {
@@ -1219,7 +1238,7 @@ k_bin_big(const int32_t* __restrict__ rows, const int64_t* __restrict__ mn, cons
     __syncwarp();
     if (prefix_words(bm, pref, 0, nwords) != m) {
 #ifdef MG_DIR_DEBUG
-      if (lane == 0) printf("bin_big mismatch row %lld h %d ja %d jb %d n %u m %u bslot %u\n", (long long)i, it.h, it.ja, it.jb, n, m, bslot);
+      if (lane == 0) printf("bin_big mismatch out %lld n %u m %u bslot %u\n", (long long)out, n, m, bslot);
 #endif
       if (lane == 0) atomicOr(err, 4ull);
       drain_first();

@@ -764,7 +764,8 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     MG_CUDA(cudaMallocAsync(&bcol[q], (size_t)std::max<int64_t>(buf_elems, 1) * 2 + 64, s));
     MG_CUDA(cudaMallocAsync(&bval[q], (size_t)std::max<int64_t>(buf_elems, 1) * 8 + 64, s));
     // windows and units: <= one per chunk entry; big-chunk parts: <= entries + elements / kBigSplit
-    MG_CUDA(cudaMallocAsync(&items[q], ((size_t)std::max<int64_t>(max_ent, 1) * 3 + (size_t)max_big) * sizeof(mg::BinItem), s));
+    MG_CUDA(cudaMallocAsync(&items[q], (size_t)std::max<int64_t>(max_ent, 1) * 3 * sizeof(mg::BinItem) +
+                                           (size_t)max_big * sizeof(mg::BigItem), s));
     MG_CUDA(cudaMallocAsync(&cnts[q], 128, s));
   }
   const size_t big_smem = mg::bin_big_smem(ctx->sem.shift_num);
@@ -811,8 +812,8 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     const int64_t h0 = cuts[b], h1 = cuts[b + 1];
     mg::BinItem* wins = static_cast<mg::BinItem*>(items[q]);
     mg::BinItem* units = wins + std::max<int64_t>(max_ent, 1);
-    mg::BinItem* bigs = units + std::max<int64_t>(max_ent, 1);
-    mg::BinItem* wins_t = bigs + max_big;   // windows of tiny chunks (k_bin_reduce_tiny)
+    mg::BinItem* wins_t = units + std::max<int64_t>(max_ent, 1);   // windows of tiny chunks (k_bin_reduce_tiny)
+    mg::BigItem* bigs = reinterpret_cast<mg::BigItem*>(wins_t + std::max<int64_t>(max_ent, 1));
     auto* nwin = static_cast<unsigned long long*>(cnts[q]);
     auto* nunit = nwin + 1;
     auto* nbig = nwin + 2;
@@ -825,7 +826,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     ctx->begin(MAGNUS_K_BIN_PLAN);
     mg::k_bin_plan<<<(unsigned)std::min<int64_t>((h1 - h0 + 7) / 8, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
         ctx->listH, h0, h1, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, wins, nwin, wins_t, bigs, nbig, units,
-        nunit, std::max<int64_t>(max_ent, 1), max_big);
+        nunit, std::max<int64_t>(max_ent, 1), max_big, ctx->cd, ctx->hbase, hb[b], c_rp, ctx->cbm_slot);
     ctx->end();
     ctx->begin(MAGNUS_K_BIN_EXPAND);
     if (exp2) {
@@ -848,8 +849,8 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     MG_CUDA(cudaStreamWaitEvent(sbig, ctx->ev_e[q], 0));
     cudaEvent_t m1 = ctx->begin_on(MAGNUS_K_BIN_BIG, sbig);
     mg::k_bin_big<<<(unsigned)(ctx->sm_count * occ_b), 32, big_smem, sbig>>>(
-        ctx->listH, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->hbase, hb[b], bigs, nbig, nwin + 5, max_big,
-        ctx->cbm_pool, ctx->cbm_slot, static_cast<const uint16_t*>(bcol[q]), static_cast<const double*>(bval[q]), c_rp, c_col, c_val, ctx->err);
+        ctx->sem, bigs, nbig, nwin + 5, max_big, ctx->cbm_pool, static_cast<const uint16_t*>(bcol[q]),
+        static_cast<const double*>(bval[q]), c_col, c_val, ctx->err);
     ctx->end_on(MAGNUS_K_BIN_BIG, m1, sbig);
     MG_CUDA(cudaEventRecord(ctx->ev_b[q], sbig));
     MG_CUDA(cudaStreamWaitEvent(sr, ctx->ev_e[q], 0));
