@@ -4,33 +4,31 @@
 // of work is independent, so all SMs stay busy.
 //
 // Chunks are the numeric plan's fine chunks (column c in chunk c >> shift_num,
-// which decides the association of every output value).  Each chunk is cut
-// into sub-bins of at most 512 columns (c >> gs).
+// which decides the association of every output value; chunk width <= 2^14).
 //
-//   symbolic (heavy_rows.cuh)  per heavy row and sub-bin: element count and
+//   symbolic (symbolic_rows.cuh)  per heavy row and chunk: product count and
 //                              distinct-column count, stored as exclusive
 //                              prefixes ce / cd (offsets in the reorder buffer
-//                              and in the C row).
-//   k_bin_plan                 cuts each row into reduce windows -- runs of
-//                              whole "small" chunks (<= kBinE elements, < 2
-//                              kBinWinT per window) or one sub-bin of a "big"
-//                              chunk -- and into expand units (chunk ranges).
-//   k_bin_expand (warp/unit)   walks the row's B rows in ascending k (Gustavson
+//                              and in the C row), and the column bitmaps of
+//                              big chunks.
+//   k_bin_plan                 cuts each row into reduce windows (runs of
+//                              small chunks), big-chunk items and expand units
+//                              (chunk ranges).
+//   k_bin_expand2 (CTA/unit)   walks the unit's B rows in ascending k (Gustavson
 //                              order, gustavson.py:44-59) and appends each
-//                              product to its slice: the whole chunk for a small
-//                              chunk, the sub-bin for a big one.  Every slice is
-//                              in ascending k: the reference's stable fine-level
+//                              product to its chunk's slice; every slice is in
+//                              ascending k: the reference's stable fine-level
 //                              scatter order (magnus.py:236-249).
-//   k_bin_reduce (warp/window) small chunk: bitmap -> column ranks, stable
-//                              counting sort of the slice into shared memory,
-//                              then per column the association the reference
-//                              gives the chunk (accumulators.py:132-134): dense
-//                              = sequential from +0.0 when the chunk holds >=
-//                              crossover elements, else sort = x0 +
-//                              pairwise(rest).  Big chunk (always dense, since
-//                              kBinE >= crossover is a precondition): each
-//                              sub-bin is accumulated in stream order into a
-//                              dense shared-memory window, as the reference's
+//   k_bin_reduce / _tiny       small chunks (<= kBinE products): stable sort of
+//   (warp/window)              the slice by column, then per column the
+//                              association the reference gives the chunk
+//                              (accumulators.py:132-134): dense = sequential
+//                              from +0.0 when the chunk holds >= crossover
+//                              elements, else sort = x0 + pairwise(rest).
+//   k_bin_big (warp/chunk)     big chunks (always the dense association, since
+//                              kBinE >= crossover is a precondition): the slice
+//                              is accumulated in stream order into a dense
+//                              shared-memory accumulator, as the reference's
 //                              dense accumulator does (accumulators.py:68-97).
 #pragma once
 #include "common.cuh"
@@ -53,13 +51,6 @@ constexpr int kBinCur = MG_BIN_CUR;   // expand: chunks per unit (cursors / coun
 #define MG_UNIT_MAX (1 << 17)
 #endif
 constexpr int64_t kBinUnitMax = MG_UNIT_MAX;   // expand: elements per unit (rows above are split by chunk ranges)
-#ifndef MG_EXP_U
-#define MG_EXP_U 8
-#endif
-#ifndef MG_EXP_MINB
-#define MG_EXP_MINB 8
-#endif
-constexpr int kBinU = MG_EXP_U;       // waves of loads in flight per lane
 constexpr uint32_t kBigSplit = 1u << 17;   // big chunks above this many elements are split by columns
 constexpr uint32_t kBigFront = 1u << 14;   // big chunks scheduled first
 constexpr uint32_t kUnitFront = 1u << 15;  // expand units scheduled first
@@ -257,209 +248,6 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
         if (um) ustart = q0 + 31 - __clz(um) + 1;
       }
     }
-  }
-}
-
-// Expand: one warp per unit; products appended to their slice in ascending k.
-__global__ void __launch_bounds__(kBinT, MG_EXP_MINB)
-k_bin_expand(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t* __restrict__ mn,
-             const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce,
-             const int64_t* __restrict__ hbase, int64_t batch_base, const BinItem* __restrict__ units,
-             const unsigned long long* __restrict__ nunit, unsigned long long* __restrict__ ticket, int64_t cap_units,
-             uint16_t* __restrict__ bcol, double* __restrict__ bval, const int32_t* __restrict__ bslot,
-             const uint32_t* __restrict__ bidx, int64_t nwin1, int ilog) {
-  __shared__ uint32_t s_cur[kBinT / 32][kBinCur];
-  __shared__ uint32_t s_big[kBinT / 32][kBinCur / 32];   // big-chunk flags of the unit's chunks
-  const int lane = threadIdx.x & 31;
-  uint32_t* cur = s_cur[threadIdx.x >> 5];
-  uint32_t* bigm = s_big[threadIdx.x >> 5];
-  const int gs = bin_shift_of(shift);
-  const uint64_t nu_front = nunit[0], nu = nu_front + nunit[5];   // nunit[5] = back counter (cnts[6])
-  const uint32_t cmask = (1u << shift) - 1u;
-  while (true) {
-    unsigned long long u = 0;
-    if (lane == 0) u = atomicAdd(ticket, 1ull);
-    u = __shfl_sync(0xffffffffu, u, 0);
-    if (u >= nu) break;
-    const BinItem it = units[list_slot(u, nu_front, cap_units)];
-    const int64_t i = rows[it.h];
-    const int64_t a0 = A.rp(i), a1 = A.rp(i + 1);
-    const RowBins rb = row_bins(mn[i], mx[i], shift);
-    const uint32_t* e = ce + choff[it.h];
-    const int nent = it.jb - it.ja;
-    for (int j = lane; j < nent; j += 32) cur[j] = __ldg(e + it.ja + j);
-    // chunks of the unit: [cfirst, clast]
-    const int64_t cfirst = (rb.b0 + it.ja) >> rb.cs, clast = (rb.b0 + it.jb - 1) >> rb.cs;
-    const int nck = (int)(clast - cfirst + 1);
-    for (int w0 = 0; w0 < nck; w0 += 32) {
-      const int r = w0 + lane;
-      bool big = false;
-      if (r < nck) {
-        const int cj = (int)(cfirst + r - rb.c0);
-        big = __ldg(e + rb.je(cj)) - __ldg(e + rb.js(cj)) > (uint32_t)kBinE;
-      }
-      const uint32_t m = __ballot_sync(0xffffffffu, big);
-      if (lane == 0) bigm[w0 >> 5] = m;
-    }
-    const int64_t rowbase = hbase[it.h] - batch_base;
-    uint16_t* rc = bcol + rowbase;
-    double* rv = bval + rowbase;
-    const uint32_t clo = (uint32_t)((rb.b0 + it.ja) << gs);
-    const int64_t chi64 = (rb.b0 + it.jb) << gs;
-    const uint32_t chi = chi64 >= ((int64_t)1 << 32) ? 0xffffffffu : (uint32_t)chi64;
-    __syncwarp();
-    // slice of column c (chunk, or sub-bin inside a big chunk), relative to the unit
-    auto slice_of = [&](uint32_t c) -> uint32_t {
-      const int64_t ck = c >> shift;
-      if (rb.cs == 0) return (uint32_t)(ck - rb.b0 - it.ja);
-      const int r = (int)(ck - cfirst);
-      const bool big = (bigm[r >> 5] >> (r & 31)) & 1u;
-      const int64_t ent = big ? (int64_t)(c >> gs) - rb.b0 : max((int64_t)0, (ck << rb.cs) - rb.b0);
-      return (uint32_t)(ent - it.ja);
-    };
-    // groups of 32 k's, in order.  A long B row (>= 32 products) is walked on its own,
-    // 32 consecutive products per wave (equal slices are contiguous runs); a run of
-    // short B rows is flattened into one stream (lane-consecutive positions), so the
-    // loads of many short rows are in flight together.
-    for (int64_t t0 = a0; t0 < a1; t0 += 32) {
-      const int64_t t = t0 + lane;
-      uint32_t p0 = 0, p1 = 0;
-      double av = 0.0;
-      if (t < a1) {
-        const int64_t k = __ldg(A.col + t);
-        av = __ldg(A.val + t);
-        p0 = (uint32_t)B.rp(k);
-        p1 = (uint32_t)B.rp(k + 1);
-        if (!it.kind) {
-          // segment of the unit's column range: one load each from the B window index
-          // (long rows; unit bounds are sub-bin aligned), else binary searches
-          const int32_t sl = __ldg(bslot + k);
-          if (sl >= 0) {
-            const uint32_t* ix = bidx + (size_t)sl * nwin1;
-            p0 = __ldg(ix + min((int64_t)(clo >> ilog), nwin1 - 1));
-            p1 = __ldg(ix + min(chi64 >> ilog, nwin1 - 1));
-          } else {
-            p0 = lower_bound_col(B.col, p0, p1, clo);
-            p1 = lower_bound_col(B.col, p0, p1, chi);
-          }
-        }
-      }
-      const uint32_t len = p1 - p0;
-      const uint32_t longm = __ballot_sync(0xffffffffu, len >= 32u);
-      int ts = 0;
-      while (ts < 32) {
-        if ((longm >> ts) & 1u) {
-          // ---- one long B row
-          const uint32_t bb0 = __shfl_sync(0xffffffffu, p0, ts), bb1 = __shfl_sync(0xffffffffu, p1, ts);
-          const double a = __shfl_sync(0xffffffffu, av, ts);
-          // software pipeline: the loads of the next 32 * kBinU products are in flight while
-          // the current ones are placed
-          uint32_t c[kBinU], cn[kBinU];
-          double v[kBinU], vn[kBinU];
-#pragma unroll
-          for (int w = 0; w < kBinU; ++w) {
-            const uint32_t pp = bb0 + w * 32 + lane;
-            c[w] = pp < bb1 ? __ldg(B.col + pp) : 0xffffffffu;
-            v[w] = pp < bb1 ? __ldg(B.val + pp) : 0.0;
-          }
-          for (uint32_t q0 = bb0; q0 < bb1; q0 += 32 * kBinU) {
-            const uint32_t q1 = q0 + 32 * kBinU;
-#pragma unroll
-            for (int w = 0; w < kBinU; ++w) {
-              const uint32_t pp = q1 + w * 32 + lane;
-              cn[w] = pp < bb1 ? __ldg(B.col + pp) : 0xffffffffu;
-              vn[w] = pp < bb1 ? __ldg(B.val + pp) : 0.0;
-            }
-#pragma unroll
-            for (int w = 0; w < kBinU; ++w) {
-              if (q0 + w * 32 < bb1) {
-                const bool valid = c[w] != 0xffffffffu;
-                const uint32_t fl = valid ? slice_of(c[w]) : (0x80000000u | lane);
-                const uint32_t prevf = __shfl_up_sync(0xffffffffu, fl, 1);
-                const uint32_t nextf = __shfl_down_sync(0xffffffffu, fl, 1);
-                const uint32_t hm = __ballot_sync(0xffffffffu, lane == 0 || prevf != fl);
-                const uint32_t rank = (uint32_t)(lane - (31 - __clz(hm & lanemask_le())));
-                const bool last = lane == 31 || nextf != fl;
-                uint32_t slot = 0;
-                if (valid) slot = cur[fl] + rank;
-                __syncwarp();
-                if (valid && last) cur[fl] = slot + 1;
-#ifdef MG_EXP_NOSTORE
-                if (valid && slot == 0xfffffff0u) {
-#else
-                if (valid) {
-#endif
-                  rc[slot] = (uint16_t)(c[w] & cmask);
-                  rv[slot] = __dmul_rn(a, v[w]);
-                }
-                __syncwarp();
-              }
-            }
-#pragma unroll
-            for (int w = 0; w < kBinU; ++w) {
-              c[w] = cn[w];
-              v[w] = vn[w];
-            }
-          }
-          ++ts;
-          continue;
-        }
-        // ---- run of short B rows [ts, te): flattened
-        const uint32_t after = longm & ~((2u << ts) - 1u) & ~(ts == 31 ? 0xffffffffu : 0u);
-        const int te = after ? __ffs(after) - 1 : 32;
-        const uint32_t lr = (lane >= ts && lane < te) ? len : 0u;
-        const uint32_t inc = warp_incl_scan(lr);
-        const uint32_t off = inc - lr;
-        const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-        for (uint32_t q0 = 0; q0 < total; q0 += 32 * kBinU) {
-          uint32_t c[kBinU], tk[kBinU];
-          double v[kBinU];
-#pragma unroll
-          for (int w = 0; w < kBinU; ++w) {
-            const uint32_t q = q0 + w * 32 + lane;
-            // segment of stream position q: last lane with off <= q (lanes outside the run have
-            // lr = 0, so the search lands on a lane of the run)
-            int lo = 0;
-#pragma unroll
-            for (int st = 16; st > 0; st >>= 1) {
-              const uint32_t o = __shfl_sync(0xffffffffu, off, lo + st);
-              if (o <= q) lo += st;
-            }
-            const uint32_t pp = __shfl_sync(0xffffffffu, p0, lo) + (q - __shfl_sync(0xffffffffu, off, lo));
-            const double a = __shfl_sync(0xffffffffu, av, lo);
-            tk[w] = (uint32_t)lo;
-            c[w] = 0xffffffffu;
-            v[w] = 0.0;
-            if (q < total) {
-              c[w] = __ldg(B.col + pp);
-              v[w] = __dmul_rn(a, __ldg(B.val + pp));
-            }
-          }
-#pragma unroll
-          for (int w = 0; w < kBinU; ++w) {
-            if (q0 + w * 32 < total) {
-              const bool valid = c[w] != 0xffffffffu;
-              const uint32_t fl = valid ? slice_of(c[w]) : (0x80000000u | lane);
-              const uint32_t peers = __match_any_sync(0xffffffffu, fl);
-              const uint32_t rank = __popc(peers & lanemask_lt());
-              const bool last = (peers >> lane) == 1u;
-              (void)tk;
-              uint32_t slot = 0;
-              if (valid) slot = cur[fl] + rank;
-              __syncwarp();
-              if (valid && last) cur[fl] = slot + 1;
-              if (valid) {
-                rc[slot] = (uint16_t)(c[w] & cmask);
-                rv[slot] = v[w];
-              }
-              __syncwarp();
-            }
-          }
-        }
-        ts = te;
-      }
-    }
-    __syncwarp();
   }
 }
 
@@ -1099,9 +887,6 @@ constexpr int kBigNS = MG_BIG_NS;          // ring stages per warp
 constexpr int kBigSE = MG_BIG_SE;          // elements per stage
 constexpr int kBigSC = kBigSE * 2 + 16;    // stage bytes: columns (+ alignment slack)
 constexpr int kBigSV = kBigSE * 8 + 16;    // stage bytes: values (+ alignment slack)
-#ifdef MG_BIG_STATS
-__device__ unsigned long long g_big_stats[8];
-#endif
 
 __host__ __device__ inline size_t bin_big_smem(int shift) {
   const size_t width = size_t(1) << shift, words = (width + 31) / 32;
@@ -1189,9 +974,6 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
     const uint32_t colbase = it.colbase;
     const uint32_t parts = (uint32_t)it.kind >> 16, part = (uint32_t)it.kind & 0xffffu;
     const uint32_t plo = (uint32_t)(((uint64_t)width * part) / parts), phi = (uint32_t)(((uint64_t)width * (part + 1)) / parts);
-#ifdef MG_BIG_STATS
-    long long t_a = clock64();
-#endif
     const uint32_t nst = (n + kBigSE - 1) / kBigSE;   // stages of one pass over the slice
     // stage j of the slice -> ring slot; copies of 16-byte aligned supersets
     auto issue = [&](uint32_t j) {
@@ -1244,10 +1026,6 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
       drain_first();
       continue;
     }
-#ifdef MG_BIG_STATS
-    long long t_b = clock64();
-    if (lane == 0) atomicAdd(&g_big_stats[4], (unsigned long long)(t_b - t_a));
-#endif
     const uint32_t rlo0 = plo < width ? rank_of(bm, pref, plo) : m;
     const uint32_t rhi0 = phi < width ? rank_of(bm, pref, phi) : m;
     // ---- sums, kBigD ranks per pass
@@ -1273,11 +1051,7 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
 #pragma unroll
         for (int w = 0; w < kBigSE / 32; ++w) {
           const uint32_t q = w * 32 + lane;
-#ifdef MG_BIG_X2
-          rr[w] = q < cnt ? (uint32_t)cs[q] % (rhi0 - rlo0 + 1) + rlo0 : 0xffffffffu;
-#else
           rr[w] = q < cnt ? rank_of(bm, pref, cs[q]) : 0xffffffffu;
-#endif
         }
 #pragma unroll
         for (int w = 0; w < kBigSE / 32; ++w) {
@@ -1286,23 +1060,10 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
           const bool valid = r >= rlo && r < rhi;
           const double v = valid ? vs[q] : 0.0;
           const uint32_t key = valid ? r - rlo : 0x10000u + lane;
-#ifndef MG_BIG_X3
           if (valid) inv[key] = cs[q];   // every contributor of a column writes the same value
-#endif
           const uint32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
           const uint32_t brk = __ballot_sync(0xffffffffu, valid && lane > 0 && key <= pk);
-#ifdef MG_BIG_STATS
-          {
-            const uint32_t vb = __ballot_sync(0xffffffffu, valid);
-            if (lane == 0) atomicAdd(&g_big_stats[0], 1ull);
-            if (lane == 0) atomicAdd(&g_big_stats[3], (unsigned long long)__popc(vb));
-          }
-#endif
-#ifdef MG_BIG_X1
-          if (true) {
-#else
           if (!brk) {
-#endif
             if (valid) acc[key] = __dadd_rn(acc[key], v);
           } else if (__popc(brk) < kBigRunSer) {
             // few ascending runs: apply them one after another
@@ -1316,10 +1077,6 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
             const uint32_t peers = __match_any_sync(0xffffffffu, key);
             const uint32_t gsz = __popc(peers);
             const uint32_t maxg = __reduce_max_sync(0xffffffffu, valid ? gsz : 0u);
-#ifdef MG_BIG_STATS
-            if (lane == 0) atomicAdd(&g_big_stats[1], 1ull);
-            if (lane == 0) atomicAdd(&g_big_stats[2], (unsigned long long)maxg);
-#endif
             const bool lead = valid && (peers & lanemask_lt()) == 0u;
             double sacc = lead ? acc[key] : 0.0;
             uint32_t rem = peers;
@@ -1337,19 +1094,11 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
         if (j + kBigNS < nst) issue(j + kBigNS);
       }
       __syncwarp();
-#ifdef MG_BIG_STATS
-      long long t_c = clock64();
-      if (lane == 0) atomicAdd(&g_big_stats[5], (unsigned long long)(t_c - t_b));
-#endif
       for (uint32_t r = rlo + lane; r < rhi; r += 32) {
         __stcs(c_col + out + r, colbase + (uint32_t)inv[r - rlo]);
         __stcs(c_val + out + r, acc[r - rlo]);
       }
       __syncwarp();
-#ifdef MG_BIG_STATS
-      t_b = clock64();
-      if (lane == 0) atomicAdd(&g_big_stats[6], (unsigned long long)(t_b - t_c));
-#endif
     }
   }
 }

@@ -774,11 +774,6 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   const size_t red_smem = mg::bin_reduce_warp_smem(ctx->sem.shift_num) * (mg::kBinT / 32);
   int occ = 1;
   MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mg::k_bin_reduce, mg::kBinT, red_smem));
-  int occ_e = 1;
-  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e, mg::k_bin_expand, mg::kBinT, 0));
-  // two-pass CTA expand (k_bin_expand2) unless MAGNUS_EXPAND=v1
-  const char* ev = std::getenv("MAGNUS_EXPAND");
-  const bool exp2 = !(ev && std::strcmp(ev, "v1") == 0);
   int occ_e2 = 1;
   MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e2, mg::k_bin_expand2, mg::kE2T, mg::Exp2Smem::kTotal));
   occ_e2 = std::max(occ_e2, 1);
@@ -829,20 +824,10 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
         nunit, std::max<int64_t>(max_ent, 1), max_big, ctx->cd, ctx->hbase, hb[b], c_rp, ctx->cbm_slot);
     ctx->end();
     ctx->begin(MAGNUS_K_BIN_EXPAND);
-    if (exp2) {
-      mg::k_bin_expand2<<<(unsigned)(ctx->sm_count * occ_e2), mg::kE2T, mg::Exp2Smem::kTotal, s>>>(
-          ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
-          nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]),
-          ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, e2scr, e2_stride, ctx->err);
-    } else {
-#ifndef MG_EXP_CTAS
-#define MG_EXP_CTAS occ_e
-#endif
-      mg::k_bin_expand<<<(unsigned)(ctx->sm_count * std::min(occ_e, MG_EXP_CTAS)), mg::kBinT, 0, s>>>(
-          ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
-          nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]),
-          ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog);
-    }
+    mg::k_bin_expand2<<<(unsigned)(ctx->sm_count * occ_e2), mg::kE2T, mg::Exp2Smem::kTotal, s>>>(
+        ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
+        nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]),
+        ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, e2scr, e2_stride, ctx->err);
     ctx->end();
     MG_CUDA(cudaEventRecord(ctx->ev_e[q], s));
     // the big-chunk and small-chunk reducers of this batch run on their own streams
@@ -1053,17 +1038,6 @@ int magnus_numeric(magnus_ctx* ctx, const int64_t* c_row_ptr, uint32_t* c_col, d
     counters->rows_fine = ctx->host_stats[mg::kStatCat + 2];
     counters->rows_coarse = ctx->host_stats[mg::kStatCat + 3];
   }
-  return MAGNUS_OK;
-}
-
-// internal debug hook: counters of the big-chunk reducer when built with -DMG_BIG_STATS
-int magnus_debug_big_stats(unsigned long long* out8) {
-#ifdef MG_BIG_STATS
-  MG_CUDA(cudaDeviceSynchronize());
-  MG_CUDA(cudaMemcpyFromSymbol(out8, mg::g_big_stats, 8 * 8));
-#else
-  for (int i = 0; i < 8; ++i) out8[i] = 0;
-#endif
   return MAGNUS_OK;
 }
 

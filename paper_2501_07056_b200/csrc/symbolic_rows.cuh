@@ -193,7 +193,6 @@ k_heavy_sym2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows
     // per-k stream offsets and B positions: shared memory, or this CTA's global scratch
     uint32_t* koff = nk <= kS2K ? ks_off : gk + (size_t)blockIdx.x * gk_stride * 2;
     uint32_t* kpos = nk <= kS2K ? ks_pos : koff + gk_stride;
-    uint64_t total = 0;
     const int64_t wmask = ~(((int64_t)1 << kS2WinLog) - 1);
     for (int64_t wlo = row_lo & wmask; wlo <= row_hi; wlo += (int64_t)1 << kS2WinLog) {
       const int64_t whi = wlo + ((int64_t)1 << kS2WinLog);
@@ -288,7 +287,6 @@ k_heavy_sym2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows
       cd[eo + nch] = td;
       counts[i] = (int64_t)td;
     }
-    (void)total;
     __syncthreads();
   }
 }
