@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -41,6 +42,16 @@ int set_err(int code, const std::string& msg) {
 #else
 #define DIR_SYNC(what) do { } while (0)
 #endif
+
+// MAGNUS_TRACE=1: host timestamps of magnus_setup's steps on stderr (synchronising)
+static void trace_point(cudaStream_t s, const char* what) {
+  static const bool on = [] { const char* e = std::getenv("MAGNUS_TRACE"); return e && std::strcmp(e, "1") == 0; }();
+  if (!on) return;
+  static auto t0 = std::chrono::steady_clock::now();
+  cudaStreamSynchronize(s);
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  fprintf(stderr, "[trace] %10.3f ms  %s\n", ms, what);
+}
 
 #define MG_CUDA(call)                                                                         \
   do {                                                                                        \
@@ -499,6 +510,7 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     return set_err(MAGNUS_INPUT, "invalid AccumThresholds");
   if (th->sort_dense_crossover > mg::kCap)
     return set_err(MAGNUS_INPUT, "sort_dense_crossover above the device batch capacity (" + std::to_string(mg::kCap) + ")");
+  trace_point(ctx->stream ? ctx->stream : (cudaStream_t)stream, "setup: enter");
   ctx->free_all();
   // per-setup allocations are gone: no pointer may survive into this setup
   ctx->cbm_slot = ctx->cbm_pool = nullptr;
@@ -562,6 +574,7 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     ctx->end();
     MG_CUDA(cudaGetLastError());
   }
+  trace_point(s, "setup: stats + categorize");
   unsigned long long hs[mg::kStatLen];
   MG_CUDA(cudaMemcpyAsync(hs, ctx->stats, sizeof hs, cudaMemcpyDeviceToHost, s));
   MG_CUDA(cudaStreamSynchronize(s));
@@ -608,21 +621,34 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   const int64_t n_chunks_global = ctx->plan_num.plan_cols >> ctx->plan_num.shift_fine;
   ctx->sem.n_chunks_num = n_chunks_global;
   ctx->sem.mode_words = (int32_t)((n_chunks_global + 31) / 32);
+  trace_point(s, "setup: coarse batches");
   // heavy-row workspace
   const int64_t nH = ctx->host_stats[mg::kStatNH];
+  MG_CUDA(ctx->alloc(&ctx->counts, n + 1));
+  MG_CUDA(ctx->alloc(&ctx->tile_sums, (n + mg::kScanTile - 1) / mg::kScanTile + 1));
   if (nH > 1) {
-    // heavy rows in ascending row order: batches then complete contiguous row ranges (the
-    // host readback overlaps them) and their contents do not depend on atomic order
-    ctx->h_rows.resize(nH);
+    // heavy rows in ascending row order (stable compaction instead of k_categorize's atomic
+    // order): batches then complete contiguous row ranges (the host readback overlaps them)
+    // and their contents do not depend on atomic order
+    int64_t* pos = nullptr;
+    MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pos), (size_t)(n + 1) * 8, s));
+    const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sm_count * 16);
+    mg::k_heavy_flags<<<g, 256, 0, s>>>(ctx->inter, n, ctx->counts);
+    const int64_t tiles = (n + mg::kScanTile - 1) / mg::kScanTile;
+    mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->counts, n, ctx->tile_sums);
+    mg::k_scan_tiles<<<1, 1024, 0, s>>>(ctx->tile_sums, tiles);
+    mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->counts, n, ctx->tile_sums, pos);
+    mg::k_heavy_scatter<<<g, 256, 0, s>>>(ctx->inter, pos, n, ctx->listH);
+    ctx->launches += 5;
+    MG_CUDA(cudaGetLastError());
+    MG_CUDA(cudaFreeAsync(pos, s));
+  }
+  ctx->h_rows.resize(nH);
+  if (nH > 0) {
     MG_CUDA(cudaMemcpyAsync(ctx->h_rows.data(), ctx->listH, nH * 4, cudaMemcpyDeviceToHost, s));
     MG_CUDA(cudaStreamSynchronize(s));
-    std::sort(ctx->h_rows.begin(), ctx->h_rows.end());
-    MG_CUDA(cudaMemcpyAsync(ctx->listH, ctx->h_rows.data(), nH * 4, cudaMemcpyHostToDevice, s));
-    MG_CUDA(cudaStreamSynchronize(s));
-  } else {
-    ctx->h_rows.assign(nH, 0);
-    if (nH == 1) MG_CUDA(cudaMemcpy(ctx->h_rows.data(), ctx->listH, 4, cudaMemcpyDeviceToHost));
   }
+  trace_point(s, "setup: heavy rows sorted");
   MG_CUDA(ctx->alloc(&ctx->modebits, std::max<int64_t>(1, nH) * ctx->sem.mode_words));
   const int64_t maxnk = ctx->host_stats[mg::kStatMaxNk];
   ctx->gk_stride = maxnk > mg::kKSN ? ((maxnk + 8) / 4) * 4 : 4;
@@ -648,8 +674,6 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   const size_t gchunk_n = (size_t)ctx->sm_count * mg::kSymCtas * ctx->ncnt * 2;
   MG_CUDA(ctx->alloc(&ctx->gchunk, chunk_global ? gchunk_n : 1));
   if (chunk_global) MG_CUDA(cudaMemsetAsync(ctx->gchunk, 0, gchunk_n * 4, s));
-  MG_CUDA(ctx->alloc(&ctx->counts, n + 1));
-  MG_CUDA(ctx->alloc(&ctx->tile_sums, (n + mg::kScanTile - 1) / mg::kScanTile + 1));
   if (ctx->binned) {
     MG_CUDA(ctx->alloc(&ctx->nent, nH));
     MG_CUDA(ctx->alloc(&ctx->hinter, nH));
@@ -688,6 +712,7 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
       MG_CUDA(ctx->alloc(&ctx->cbm_pool, (size_t)ctx->cbm_cap * wpc));
     }
   }
+  trace_point(s, "setup: chunk tables allocated");
   if (ctx->direct) {
     int rc2 = setup_direct(ctx);
     if (rc2) return rc2;
@@ -695,6 +720,7 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     int rc2 = setup_bidx(ctx, ctx->gshift);   // expand units start and end on sub-bin boundaries
     if (rc2) return rc2;
   }
+  trace_point(s, "setup: B window index");
   ctx->ready = true;
   return MAGNUS_OK;
 }
@@ -888,7 +914,9 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
   const int64_t nH = ctx->host_stats[mg::kStatNH];
   // the light row classes run on a side stream, concurrently with the heavy rows
   const char* serial_env = std::getenv("MAGNUS_SERIAL");
-  const bool side = nH > 0 && serial_env && std::strcmp(serial_env, "0") == 0;
+  // (light rows on a side stream while the heavy rows compute; MAGNUS_LIGHT_SIDE=0 serialises)
+  const char* light_env = std::getenv("MAGNUS_LIGHT_SIDE");
+  const bool side = nH > 0 && ((serial_env && std::strcmp(serial_env, "0") == 0) || !(light_env && std::strcmp(light_env, "0") == 0));
   if (side) {
     MG_CUDA(cudaEventRecord(ctx->ev_fork, s));
     MG_CUDA(cudaStreamWaitEvent(ctx->aux3, ctx->ev_fork, 0));

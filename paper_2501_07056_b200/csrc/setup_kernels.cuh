@@ -94,6 +94,18 @@ __global__ void k_categorize(int64_t n, DevCsr A, const int64_t* __restrict__ in
   }
 }
 
+// heavy rows (> kBlockMax products) in ascending row order: flags for an exclusive scan ...
+__global__ void k_heavy_flags(const int64_t* __restrict__ inter, int64_t n, int64_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = inter[i] > kBlockMax ? 1 : 0;
+}
+// ... and the scatter to the scanned positions
+__global__ void k_heavy_scatter(const int64_t* __restrict__ inter, const int64_t* __restrict__ pos, int64_t n,
+                                int32_t* __restrict__ listH) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (inter[i] > kBlockMax) listH[pos[i]] = (int32_t)i;
+}
+
 // skip list of B: skip[j] = col[32*j]
 __global__ void k_build_skip(const uint32_t* __restrict__ col, int64_t nnz, uint32_t* __restrict__ skip) {
   const int64_t n = (nnz + 31) / 32;
