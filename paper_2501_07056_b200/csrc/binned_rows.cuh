@@ -55,6 +55,11 @@ constexpr uint32_t kBigSplit = 1u << 17;   // big chunks above this many element
 constexpr uint32_t kBigFront = 1u << 14;   // big chunks scheduled first
 constexpr uint32_t kUnitFront = 1u << 15;  // expand units scheduled first
 constexpr int kBigMaxParts = 32;
+#ifndef MG_BIG_D
+#define MG_BIG_D 1024
+#endif
+constexpr int kBigD = MG_BIG_D;            // ranks accumulated per pass
+
 
 __host__ __device__ inline int bin_shift_of(int shift_num) { return shift_num < kSubShift ? shift_num : kSubShift; }
 
@@ -217,19 +222,26 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
       if (big) {
         const int parts = (int)min((uint32_t)kBigMaxParts, (n + kBigSplit - 1) / kBigSplit);
         const bool large = n >= kBigFront;
-        const unsigned long long b0i = atomicAdd(large ? nbig : nbig_back, (unsigned long long)parts);
+        // chunks with more distinct columns than one kBigD pass go to the wide-accumulator list
+        const uint32_t* dd = cd + choff[h];
+        const uint32_t mcols = __ldg(dd + je) - __ldg(dd + js);
+        const bool wide = mcols > (uint32_t)kBigD;
+        BigItem* bl = wide ? bigs + cap_bigs : bigs;
+        unsigned long long* cf = wide ? nwin + 10 : nbig;
+        unsigned long long* cb = wide ? nwin + 15 : nbig_back;
+        const unsigned long long b0i = atomicAdd(large ? cf : cb, (unsigned long long)parts);
         const uint32_t* d = cd + choff[h];
         BigItem bi;
         bi.slice = hbase[h] - batch_base + pe;
         bi.out = c_rp[i] + __ldg(d + js);
         bi.n = n;
-        bi.m = __ldg(d + je) - __ldg(d + js);
+        bi.m = mcols;
         bi.colbase = (uint32_t)(((rb.b0 + js) >> rb.cs) << shift);
         bi.bslot = cbm_slot != nullptr ? __ldg(cbm_slot + choff[h] + js) : 0xffffffffu;
         bi.pad = 0;
         for (int pp = 0; pp < parts; ++pp) {
           bi.kind = ((uint32_t)parts << 16) | (uint32_t)pp;
-          bigs[large ? (int64_t)(b0i + pp) : cap_bigs - 1 - (int64_t)(b0i + pp)] = bi;
+          bl[large ? (int64_t)(b0i + pp) : cap_bigs - 1 - (int64_t)(b0i + pp)] = bi;
         }
       }
       // ---- expand units: chunk ranges (whole chunks, so small-chunk slices stay in one unit)
@@ -869,10 +881,6 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
 // asynchronous bulk copies (cp.async.bulk, completion on an mbarrier), so many
 // bytes per warp are in flight without registers.  Chunks above kBigSplit
 // elements are split into column parts handled by different warps.
-#ifndef MG_BIG_D
-#define MG_BIG_D 1024
-#endif
-constexpr int kBigD = MG_BIG_D;            // ranks accumulated per pass
 #ifndef MG_BIG_RS
 #define MG_BIG_RS 3
 #endif
@@ -888,9 +896,14 @@ constexpr int kBigSE = MG_BIG_SE;          // elements per stage
 constexpr int kBigSC = kBigSE * 2 + 16;    // stage bytes: columns (+ alignment slack)
 constexpr int kBigSV = kBigSE * 8 + 16;    // stage bytes: values (+ alignment slack)
 
-__host__ __device__ inline size_t bin_big_smem(int shift) {
+#ifndef MG_BIG_DW
+#define MG_BIG_DW 2048
+#endif
+constexpr int kBigDWide = MG_BIG_DW;            // ranks per pass for chunks with more than kBigD columns
+
+__host__ __device__ inline size_t bin_big_smem(int shift, int D = kBigD) {
   const size_t width = size_t(1) << shift, words = (width + 31) / 32;
-  return (size_t)kBigD * 8 + (size_t)kBigD * 2 + ((words * 4 + 15) & ~size_t(15)) + ((words * 2 + 15) & ~size_t(15)) +
+  return (size_t)D * 8 + (size_t)D * 2 + ((words * 4 + 15) & ~size_t(15)) + ((words * 2 + 15) & ~size_t(15)) +
          (size_t)kBigNS * (kBigSC + kBigSV) + kBigNS * 8;
 }
 
@@ -933,6 +946,7 @@ struct BigStage {
   const double* v;
 };
 
+template <int D>
 __global__ void __launch_bounds__(32)
 k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* __restrict__ nbig,
           unsigned long long* __restrict__ ticket, int64_t cap_bigs,
@@ -943,11 +957,11 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
   const uint32_t width = 1u << shift;
   const int nwords = (int)((width + 31) / 32);
   unsigned char* sp = smem;
-  double* acc = reinterpret_cast<double*>(sp); sp += (size_t)kBigD * 8;
+  double* acc = reinterpret_cast<double*>(sp); sp += (size_t)D * 8;
   unsigned char* stv0 = sp; sp += (size_t)kBigNS * kBigSV;   // 16-byte aligned (kBigD * 8 is)
   unsigned char* stc0 = sp; sp += (size_t)kBigNS * kBigSC;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sp); sp += kBigNS * 8;
-  uint16_t* inv = reinterpret_cast<uint16_t*>(sp); sp += (size_t)kBigD * 2;   // rank - rlo -> column
+  uint16_t* inv = reinterpret_cast<uint16_t*>(sp); sp += (size_t)D * 2;   // rank - rlo -> column
   uint32_t* bm = reinterpret_cast<uint32_t*>(sp); sp += ((size_t)nwords * 4 + 15) & ~size_t(15);
   uint16_t* pref = reinterpret_cast<uint16_t*>(sp);
   const int lane = threadIdx.x & 31;
@@ -1028,10 +1042,10 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
     }
     const uint32_t rlo0 = plo < width ? rank_of(bm, pref, plo) : m;
     const uint32_t rhi0 = phi < width ? rank_of(bm, pref, phi) : m;
-    // ---- sums, kBigD ranks per pass
+    // ---- sums, D ranks per pass
     if (rlo0 >= rhi0) drain_first();
-    for (uint32_t rlo = rlo0; rlo < rhi0; rlo += kBigD) {
-      const uint32_t rhi = min(rhi0, rlo + kBigD);
+    for (uint32_t rlo = rlo0; rlo < rhi0; rlo += D) {
+      const uint32_t rhi = min(rhi0, rlo + D);
       for (uint32_t r = lane; r < rhi - rlo; r += 32) acc[r] = 0.0;
       uint32_t u0 = u_first;   // ring use index of stage 0 of this pass
       if (rlo != rlo0) {

@@ -337,8 +337,10 @@ int magnus_ctx_create(magnus_ctx** out) {
                                (int)mg::HeavyNumSmem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_bin_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)(mg::bin_reduce_warp_smem(mg::kBinMaxShift) * (mg::kBinT / 32))));
-  MG_CUDA(cudaFuncSetAttribute(mg::k_bin_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)mg::bin_big_smem(mg::kBinMaxShift)));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_bin_big<mg::kBigD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)mg::bin_big_smem(mg::kBinMaxShift, mg::kBigD)));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_bin_big<mg::kBigDWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)mg::bin_big_smem(mg::kBinMaxShift, mg::kBigDWide)));
   MG_CUDA(cudaFuncSetAttribute(mg::k_bin_expand2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::Exp2Smem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_heavy_sym2, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -791,12 +793,16 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     MG_CUDA(cudaMallocAsync(&bval[q], (size_t)std::max<int64_t>(buf_elems, 1) * 8 + 64, s));
     // windows and units: <= one per chunk entry; big-chunk parts: <= entries + elements / kBigSplit
     MG_CUDA(cudaMallocAsync(&items[q], (size_t)std::max<int64_t>(max_ent, 1) * 3 * sizeof(mg::BinItem) +
-                                           (size_t)max_big * sizeof(mg::BigItem), s));
+                                           (size_t)max_big * 2 * sizeof(mg::BigItem), s));
     MG_CUDA(cudaMallocAsync(&cnts[q], 128, s));
   }
-  const size_t big_smem = mg::bin_big_smem(ctx->sem.shift_num);
-  int occ_b = 1;
-  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, mg::k_bin_big, 32, big_smem));
+  const size_t big_smem = mg::bin_big_smem(ctx->sem.shift_num, mg::kBigD);
+  const size_t big_smem_w = mg::bin_big_smem(ctx->sem.shift_num, mg::kBigDWide);
+  int occ_b = 1, occ_bw = 1;
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, mg::k_bin_big<mg::kBigD>, 32, big_smem));
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_bw, mg::k_bin_big<mg::kBigDWide>, 32, big_smem_w));
+  occ_b = std::max(occ_b, 1);
+  occ_bw = std::max(occ_bw, 1);
   const size_t red_smem = mg::bin_reduce_warp_smem(ctx->sem.shift_num) * (mg::kBinT / 32);
   int occ = 1;
   MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mg::k_bin_reduce, mg::kBinT, red_smem));
@@ -859,8 +865,12 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     // the big-chunk and small-chunk reducers of this batch run on their own streams
     MG_CUDA(cudaStreamWaitEvent(sbig, ctx->ev_e[q], 0));
     cudaEvent_t m1 = ctx->begin_on(MAGNUS_K_BIN_BIG, sbig);
-    mg::k_bin_big<<<(unsigned)(ctx->sm_count * occ_b), 32, big_smem, sbig>>>(
+    mg::k_bin_big<mg::kBigD><<<(unsigned)(ctx->sm_count * occ_b), 32, big_smem, sbig>>>(
         ctx->sem, bigs, nbig, nwin + 5, max_big, ctx->cbm_pool, static_cast<const uint16_t*>(bcol[q]),
+        static_cast<const double*>(bval[q]), c_col, c_val, ctx->err);
+    // chunks with more than kBigD distinct columns: one pass with a 4096-rank accumulator
+    mg::k_bin_big<mg::kBigDWide><<<(unsigned)(ctx->sm_count * occ_bw), 32, big_smem_w, sbig>>>(
+        ctx->sem, bigs + max_big, nwin + 10, nwin + 12, max_big, ctx->cbm_pool, static_cast<const uint16_t*>(bcol[q]),
         static_cast<const double*>(bval[q]), c_col, c_val, ctx->err);
     ctx->end_on(MAGNUS_K_BIN_BIG, m1, sbig);
     MG_CUDA(cudaEventRecord(ctx->ev_b[q], sbig));
