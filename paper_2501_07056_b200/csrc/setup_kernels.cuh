@@ -43,7 +43,10 @@ __global__ void k_row_stats(DevCsr A, DevCsr B, int64_t* __restrict__ inter, int
 // Device row classes (execution strategy only; results never depend on them).
 constexpr int kClsNone = -1, kClsWarp = 0, kClsBlock = 1, kClsHeavy = 2;
 constexpr int64_t kWarpMax = 256;    // <= 256 intermediate elements: one warp, smem bitonic
-constexpr int64_t kBlockMax = 4096;  // <= 4096: one CTA, smem bitonic
+#ifndef MG_BLOCK_MAX
+#define MG_BLOCK_MAX 4096
+#endif
+constexpr int64_t kBlockMax = MG_BLOCK_MAX;  // <= kBlockMax products: one CTA per row (smem merge)
 
 struct CatParams {
   int64_t crossover;   // sort_dense_crossover
