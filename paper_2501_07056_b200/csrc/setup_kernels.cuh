@@ -63,37 +63,68 @@ constexpr int kStatCat = 0, kStatInter = 4, kStatMaxNk = 5, kStatNW = 6, kStatNB
 constexpr int64_t kDenseRangeMax = 32768, kDenseInterMax = 1024;
 
 // categorize_rows (reference magnus.py:68-94): first matching rule wins.
-// Also bins rows into the device execution classes and lists coarse rows.
+// Also bins rows into the device execution classes and lists coarse rows.  Counters and
+// list appends are warp-aggregated (one atomic per warp and counter: millions of rows).
+__device__ __forceinline__ void warp_append(bool flag, int32_t value, int32_t* __restrict__ list,
+                                            unsigned long long* __restrict__ count) {
+  const uint32_t m = __ballot_sync(0xffffffffu, flag);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long b = 0;
+  if (lane == 0) b = atomicAdd(count, (unsigned long long)__popc(m));
+  b = __shfl_sync(0xffffffffu, b, 0);
+  if (flag) list[b + __popc(m & ((1u << lane) - 1u))] = value;
+}
+
 __global__ void k_categorize(int64_t n, DevCsr A, const int64_t* __restrict__ inter, const int64_t* __restrict__ mn,
                              const int64_t* __restrict__ mx, CatParams p, int8_t* __restrict__ cat,
                              int32_t* __restrict__ listW, int32_t* __restrict__ listB, int32_t* __restrict__ listH,
                              int32_t* __restrict__ listCoarse, int32_t* __restrict__ listD,
                              unsigned long long* __restrict__ stats) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = inter[i];
-    const int64_t range = mx[i] - mn[i] + 1;
-    int c;
-    if (s < p.crossover) c = kCatSort;
-    else if (range * (p.val_bytes + 1) <= p.l2_bytes) c = kCatDense;
-    else c = p.use_coarse ? kCatCoarse : kCatFine;
-    cat[i] = (int8_t)c;
-    atomicAdd(&stats[kStatCat + c], 1ull);
-    atomicAdd(&stats[kStatInter], (unsigned long long)s);
-    if (c == kCatCoarse) {
-      unsigned long long slot = atomicAdd(&stats[kStatNCoarse], 1ull);
-      listCoarse[slot] = (int32_t)i;
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  unsigned long long ccount[4] = {0, 0, 0, 0}, isum = 0, maxnk = 0;
+  for (int64_t base = w0; base < n; base += stride) {
+    const int64_t i = base + lane;
+    const bool valid = i < n;
+    int64_t s = 0;
+    int c = -1;
+    if (valid) {
+      s = inter[i];
+      const int64_t range = mx[i] - mn[i] + 1;
+      if (s < p.crossover) c = kCatSort;
+      else if (range * (p.val_bytes + 1) <= p.l2_bytes) c = kCatDense;
+      else c = p.use_coarse ? kCatCoarse : kCatFine;
+      cat[i] = (int8_t)c;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ccount[q] += c == q ? 1ull : 0ull;
+      isum += (unsigned long long)s;
     }
-    if (s == 0) continue;
-    if (c == kCatDense && range <= kDenseRangeMax && s <= kDenseInterMax) {
-      listD[atomicAdd(&stats[kStatND], 1ull)] = (int32_t)i;
-    } else if (s <= kWarpMax) {
-      listW[atomicAdd(&stats[kStatNW], 1ull)] = (int32_t)i;
-    } else if (s <= kBlockMax) {
-      listB[atomicAdd(&stats[kStatNB], 1ull)] = (int32_t)i;
-    } else {
-      listH[atomicAdd(&stats[kStatNH], 1ull)] = (int32_t)i;
-      atomicMax(&stats[kStatMaxNk], (unsigned long long)(A.rp(i + 1) - A.rp(i)));
-    }
+    warp_append(c == kCatCoarse, (int32_t)i, listCoarse, &stats[kStatNCoarse]);
+    const bool any = valid && s > 0;
+    const bool isD = any && c == kCatDense && (mx[i] - mn[i] + 1) <= kDenseRangeMax && s <= kDenseInterMax;
+    const bool isW = any && !isD && s <= kWarpMax;
+    const bool isB = any && !isD && !isW && s <= kBlockMax;
+    const bool isH = any && !isD && !isW && !isB;
+    warp_append(isD, (int32_t)i, listD, &stats[kStatND]);
+    warp_append(isW, (int32_t)i, listW, &stats[kStatNW]);
+    warp_append(isB, (int32_t)i, listB, &stats[kStatNB]);
+    warp_append(isH, (int32_t)i, listH, &stats[kStatNH]);
+    if (isH) maxnk = max(maxnk, (unsigned long long)(A.rp(i + 1) - A.rp(i)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ccount[q] += __shfl_xor_sync(0xffffffffu, ccount[q], o);
+    isum += __shfl_xor_sync(0xffffffffu, isum, o);
+    maxnk = max(maxnk, __shfl_xor_sync(0xffffffffu, maxnk, o));
+  }
+  if (lane == 0) {
+    for (int q = 0; q < 4; ++q)
+      if (ccount[q]) atomicAdd(&stats[kStatCat + q], ccount[q]);
+    if (isum) atomicAdd(&stats[kStatInter], isum);
+    if (maxnk) atomicMax(&stats[kStatMaxNk], maxnk);
   }
 }
 
