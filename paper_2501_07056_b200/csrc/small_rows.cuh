@@ -57,6 +57,111 @@ __device__ __forceinline__ bool seq_mode(int cat, const Sem& sem, const F& chunk
   return chunk_count() >= sem.crossover;
 }
 
+// ---------------------------------------------------------------- register path (<= 64 products)
+// Gathers the row's product (<= 32 B rows, <= 64 elements; lane l holds positions l and l+32),
+// sorts (column, position) keys with a register bitonic network, and -- when no column
+// repeats (the common case: the product of two random sparse rows) -- writes C directly:
+// a single contribution is x0 under the sort association and +0.0 + x0 under the dense one.
+// Returns 0 when a column repeats: the sorted keys and the values are then left in shared
+// memory for the general path.
+template <bool Numeric>
+__device__ __forceinline__ int reg_row64(const DevCsr& B, int64_t b0, uint32_t inc, uint32_t len, double av, uint32_t nn,
+                                         unsigned long long* keys, double* vals, int ci, const Sem& sem,
+                                         int64_t* __restrict__ counts, int64_t i, int64_t out0, int64_t out1,
+                                         uint32_t* __restrict__ c_col, double* __restrict__ c_val,
+                                         unsigned long long* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t off = inc - len;
+  unsigned long long k0, k1;
+  double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const uint32_t q = (uint32_t)(r * 32 + lane);
+    int lo = 0;   // segment of q: last lane with off <= q
+#pragma unroll
+    for (int st = 16; st > 0; st >>= 1) {
+      const uint32_t o = __shfl_sync(0xffffffffu, off, lo + st);
+      if (o <= q) lo += st;
+    }
+    const int64_t bb = __shfl_sync(0xffffffffu, b0, lo);
+    const uint32_t oo = __shfl_sync(0xffffffffu, off, lo);
+    const double a = __shfl_sync(0xffffffffu, av, lo);
+    unsigned long long key = ~0ull;
+    double v = 0.0;
+    if (q < nn) {
+      const int64_t pp = bb + (q - oo);
+      key = ((unsigned long long)__ldg(B.col + pp) << 8) | q;
+      if (Numeric) v = __dmul_rn(a, __ldg(B.val + pp));
+    }
+    if (r == 0) { k0 = key; v0 = v; } else { k1 = key; v1 = v; }
+  }
+  // bitonic sort of 64 keys: element e = r * 32 + lane
+#pragma unroll
+  for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j == 32) {
+        const unsigned long long lo = k0 < k1 ? k0 : k1, hi = k0 < k1 ? k1 : k0;
+        k0 = lo;
+        k1 = hi;
+      } else {
+        const unsigned long long p0 = __shfl_xor_sync(0xffffffffu, k0, j), p1 = __shfl_xor_sync(0xffffffffu, k1, j);
+        const bool lower = (lane & j) == 0;
+        const bool up0 = (lane & k) == 0 || k == 64, up1 = ((lane + 32) & k) == 0 || k == 64;
+        const bool t0 = lower ? (up0 ? p0 < k0 : p0 > k0) : (up0 ? p0 > k0 : p0 < k0);
+        const bool t1 = lower ? (up1 ? p1 < k1 : p1 > k1) : (up1 ? p1 > k1 : p1 < k1);
+        if (t0) k0 = p0;
+        if (t1) k1 = p1;
+      }
+    }
+  }
+  const unsigned long long c0 = k0 >> 8, c1 = k1 >> 8;
+  const unsigned long long pc0 = __shfl_up_sync(0xffffffffu, c0, 1), pc1 = __shfl_up_sync(0xffffffffu, c1, 1);
+  const unsigned long long last0 = __shfl_sync(0xffffffffu, c0, 31);
+  const bool ok0 = (uint32_t)lane < nn, ok1 = (uint32_t)(lane + 32) < nn;
+  const bool h0 = ok0 && (lane == 0 || pc0 != c0);
+  const bool h1 = ok1 && (lane == 0 ? last0 != c1 : pc1 != c1);
+  const uint32_t m0 = __ballot_sync(0xffffffffu, h0), m1 = __ballot_sync(0xffffffffu, h1);
+  const uint32_t distinct = __popc(m0) + __popc(m1);
+  const bool nodup = distinct == nn;
+  if (!Numeric) {
+    if (lane == 0) counts[i] = distinct;
+    return 1;
+  }
+  if (nodup) {
+    // (a Fine / Coarse row would need its chunk counts: only Sort / Dense rows take this path)
+    if (ci == kCatSort || ci == kCatDense) {
+      const uint32_t q0 = (uint32_t)(k0 & 0xFF), q1 = (uint32_t)(k1 & 0xFF);
+      const double a0 = __shfl_sync(0xffffffffu, v0, q0 & 31), a1 = __shfl_sync(0xffffffffu, v1, q0 & 31);
+      const double b0v = __shfl_sync(0xffffffffu, v0, q1 & 31), b1v = __shfl_sync(0xffffffffu, v1, q1 & 31);
+      double x0 = q0 < 32 ? a0 : a1, x1 = q1 < 32 ? b0v : b1v;
+      if (ci == kCatDense) {
+        x0 = __dadd_rn(0.0, x0);
+        x1 = __dadd_rn(0.0, x1);
+      }
+      if (out1 - out0 != (int64_t)nn) {
+        if (lane == 0) atomicOr(err, 1ull);
+        return 1;
+      }
+      if (ok0) {
+        c_col[out0 + lane] = (uint32_t)c0;
+        c_val[out0 + lane] = x0;
+      }
+      if (ok1) {
+        c_col[out0 + 32 + lane] = (uint32_t)c1;
+        c_val[out0 + 32 + lane] = x1;
+      }
+      return 1;
+    }
+  }
+  // general path: sorted keys and the values (by position) to shared memory
+  keys[lane] = k0;
+  keys[lane + 32] = k1;
+  vals[lane] = v0;
+  vals[lane + 32] = v1;
+  return 0;
+}
+
 // ================================================================ warp per row
 constexpr int kWT = 256;  // threads per block (8 warps, one row each)
 constexpr int kWSlots = 256;
@@ -69,6 +174,7 @@ __global__ void __launch_bounds__(kWT) k_rows_warp(DevCsr A, DevCsr B, const int
   // per warp: keys (u64) + vals (f64)
   __shared__ unsigned long long s_keys[kWT / 32][kWSlots];
   __shared__ double s_vals[kWT / 32][kWSlots];
+  __shared__ int s_n[kWT / 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   unsigned long long* keys = s_keys[wib];
   double* vals = s_vals[wib];
@@ -78,6 +184,29 @@ __global__ void __launch_bounds__(kWT) k_rows_warp(DevCsr A, DevCsr B, const int
   for (int64_t w = warp; w < nrows; w += nwarps) {
     const int64_t i = rows[w];
     const int64_t a0 = A.rp(i), a1 = A.rp(i + 1);
+    if (a1 - a0 <= 32) {
+      // <= 32 k's: row lengths in one wave; a product of <= 64 elements is sorted in registers
+      const int64_t t = a0 + lane;
+      int64_t b0 = 0;
+      uint32_t len = 0;
+      double av = 0.0;
+      if (t < a1) {
+        const int64_t k = __ldg(A.col + t);
+        b0 = B.rp(k);
+        len = (uint32_t)(B.rp(k + 1) - b0);
+        if (Numeric) av = __ldg(A.val + t);
+      }
+      const uint32_t inc = warp_incl_scan(len);
+      const uint32_t nn = __shfl_sync(0xffffffffu, inc, 31);
+      if (nn <= 64u) {
+        const int st = reg_row64<Numeric>(B, b0, inc, len, av, nn, keys, vals, cat[i], sem, counts, i,
+                                           Numeric ? c_rp[i] : 0, Numeric ? c_rp[i + 1] : 0, c_col, c_val, err);
+        if (st) continue;   // done in registers (else: keys / vals sorted in shared memory)
+        if (lane == 0) s_n[wib] = (int)nn;
+        goto heads;
+      }
+    }
+    {
     // gather in Gustavson order; position p = stream index (ascending k)
     int base = 0;
     for (int64_t t0 = a0; t0 < a1; t0 += 32) {
@@ -102,10 +231,15 @@ __global__ void __launch_bounds__(kWT) k_rows_warp(DevCsr A, DevCsr B, const int
       base += __shfl_sync(0xffffffffu, inc, 31);
     }
     const int n = base;
+    s_n[wib] = n;
     const int np2 = pow2_at_least(n, 32);
     for (int p = n + lane; p < np2; p += 32) keys[p] = ~0ull;
     __syncwarp();
     bitonic<32, true>(keys, np2, lane);
+    }
+  heads:
+    __syncwarp();
+    const int n = s_n[wib];
     // column heads, ranks
     int rank_base = 0;
     const int ci = Numeric ? (int)cat[i] : 0;
