@@ -446,7 +446,7 @@ def run_e2e(A, B, sysp, steps, total_inter):
     del rp
     out_rp, out_col, out_val = HostBuffer(A.n_rows + 1, np.int64), HostBuffer(nnz, np.int32), HostBuffer(nnz, np.float64)
     times = []
-    for _ in range(steps):
+    for it in range(steps + 1):                       # (the first, untimed, warms the memory pool)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         plan = MagnusPlan(Ah, Bh, sys=sysp)           # H2D of the host inputs inside
@@ -455,7 +455,8 @@ def run_e2e(A, B, sysp, steps, total_inter):
         # C's col / val are read back while later heavy-row batches compute
         C, _ = plan.numeric(rp, host_out=(out_col.t, out_val.t))
         torch.cuda.synchronize()
-        times.append(time.perf_counter() - t0)
+        if it:
+            times.append(time.perf_counter() - t0)
         plan.close()
         del C, rp
     d2h = (A.n_rows + 1) * 8 + nnz * 12
