@@ -284,7 +284,7 @@ constexpr int kE2K = MG_E2_K;              // k's whose segments live in shared 
 constexpr int kE2U = MG_E2_U;              // waves in flight per warp
 struct Exp2Smem {
   static constexpr size_t kCnt = (size_t)kE2W * kBinCur * 4;            // per warp, per chunk of the unit
-  static constexpr size_t kK = (size_t)(kE2K + 32) * (4 + 4 + 8);       // koff, kpos, kav
+  static constexpr size_t kK = (size_t)(kE2K + 32) * (4 + 4 + 8 + 4);   // koff, kpos, kav, kslot
   static constexpr size_t kScratch = 64 * 8;
   static constexpr size_t kTotal = kCnt + kK + kScratch;
 };
@@ -328,10 +328,11 @@ struct E2Cursor {
   }
 };
 
-template <class KP, class KA>
-__device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA kav, int nk, uint32_t T, int shift, uint32_t cb,
-                                          uint32_t* cnt, const uint32_t* __restrict__ e, int ja, int nent,
-                                          uint16_t* __restrict__ rc, double* __restrict__ rv, uint32_t* scratch) {
+template <class KP, class KA, class KS>
+__device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA kav, KS kslot, int nk, uint32_t T, int shift,
+                                          uint32_t cb, uint32_t* cnt, const uint32_t* __restrict__ e, int ja, int nent,
+                                          uint16_t* __restrict__ rc, double* __restrict__ rv,
+                                          const uint32_t* __restrict__ bidx, int64_t nwin1, uint32_t* scratch) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t L = ((T + kE2W - 1) / kE2W + 31) & ~31u;
   const uint32_t q_beg = min(T, (uint32_t)wid * L), q_end = min(T, q_beg + L);
@@ -339,23 +340,26 @@ __device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA 
   const uint32_t a_wc = (uint32_t)__cvta_generic_to_shared(wc);
   const uint32_t lt = lanemask_lt(), le = lanemask_le();
   const uint32_t cmask = (1u << shift) - 1u;
-  // ---- pass 1: products per chunk of this warp's range
-  if (q_beg < q_end) {
+  // ---- pass 1: products per chunk of this warp's range.  A B row segment that lies wholly
+  // in the range and holds more elements than the unit has chunks is counted from the B
+  // window index (one difference per chunk); the other positions column by column.
+  auto count_range = [&](uint32_t qa, uint32_t qb) {
+    if (qa >= qb) return;
     E2Cursor<KP> cur{koff, kpos, nk, 0, 0, 0};
-    cur.init(q_beg);
-    for (uint32_t q00 = q_beg; q00 < q_end; q00 += 32 * kE2U) {
+    cur.init(qa);
+    for (uint32_t q00 = qa; q00 < qb; q00 += 32 * kE2U) {
       uint32_t cw[kE2U];
 #pragma unroll
       for (int u = 0; u < kE2U; ++u) {
         const uint32_t q0 = q00 + 32 * u, q = q0 + lane;
         uint32_t pos;
         int seg;
-        cur.wave(q0, q, q_end, pos, seg);
-        cw[u] = q < q_end ? __ldg(B.col + pos) : 0xffffffffu;
+        cur.wave(q0, q, qb, pos, seg);
+        cw[u] = q < qb ? __ldg(B.col + pos) : 0xffffffffu;
       }
 #pragma unroll
       for (int u = 0; u < kE2U; ++u) {
-        if (q00 + 32 * u >= q_end) break;
+        if (q00 + 32 * u >= qb) break;
         const bool valid = cw[u] != 0xffffffffu;
         const uint32_t ch = valid ? (cw[u] >> shift) - cb : 0xffffffffu;
         const uint32_t pch = __shfl_up_sync(0xffffffffu, ch, 1);
@@ -366,6 +370,32 @@ __device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA 
         sh_red_add_pred(valid && head, a_wc + (ch << 2), nxt - (uint32_t)lane);
       }
     }
+  };
+  if (q_beg < q_end) {
+    // segment of q_beg
+    int lo = 0, hi = nk;   // koff[lo] <= q_beg < koff[hi]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (koff[mid] <= q_beg) lo = mid; else hi = mid;
+    }
+    uint32_t q = q_beg;   // positions below q are counted
+    for (int j = lo; j < nk && koff[j] < q_end; ++j) {
+      const uint32_t qa = max(q_beg, (uint32_t)koff[j]), qb = min(q_end, (uint32_t)koff[j + 1]);
+      const int32_t sl = (int32_t)kslot[j];
+      if (sl < 0 || qb - qa < 64u) continue;
+      // the piece [P0, P1) of B row j inside this range: chunks c0..c1 of the unit
+      const uint32_t P0 = kpos[j] + (qa - koff[j]), P1 = P0 + (qb - qa);
+      const uint32_t c0 = (__ldg(B.col + P0) >> shift) - cb, c1 = (__ldg(B.col + P1 - 1) >> shift) - cb;
+      if (c1 - c0 + 1 > qb - qa) continue;   // sparser than one element per chunk: count columns
+      count_range(q, qa);
+      const uint32_t* ix = bidx + (size_t)sl * nwin1 + cb;
+      for (uint32_t c = c0 + lane; c <= c1; c += 32) {
+        const uint32_t lo_c = max(P0, __ldg(ix + c)), hi_c = min(P1, __ldg(ix + c + 1));
+        sh_red_add_pred(hi_c > lo_c, a_wc + (c << 2), hi_c - lo_c);
+      }
+      q = qb;
+    }
+    count_range(q, q_end);
   }
   __syncthreads();
   // ---- slice starts: chunk start (row-relative, from the symbolic tables) + earlier warps
@@ -447,6 +477,7 @@ k_bin_expand2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_
   double* s_kav = reinterpret_cast<double*>(smem + Exp2Smem::kCnt);
   uint32_t* s_koff = reinterpret_cast<uint32_t*>(smem + Exp2Smem::kCnt + (size_t)(kE2K + 32) * 8);
   uint32_t* s_kpos = s_koff + kE2K + 32;
+  uint32_t* s_kslot = s_kpos + kE2K + 32;
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + Exp2Smem::kCnt + Exp2Smem::kK);
   __shared__ unsigned long long s_u;
   const uint64_t nu_front = nunit[0], nu = nu_front + nunit[5];
@@ -467,14 +498,16 @@ k_bin_expand2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_
     const int64_t chi64 = (rb.b0 + it.jb) << shift;
     const uint32_t chi = chi64 >= ((int64_t)1 << 32) ? 0xffffffffu : (uint32_t)chi64;
     const bool big_nk = nk > kE2K;
-    uint32_t* koff = big_nk ? gk + (size_t)blockIdx.x * gk_stride * 4 : s_koff;
+    uint32_t* koff = big_nk ? gk + (size_t)blockIdx.x * gk_stride * 5 : s_koff;
     uint32_t* kpos = big_nk ? koff + gk_stride : s_kpos;
     double* kav = big_nk ? reinterpret_cast<double*>(koff + 2 * gk_stride) : s_kav;
+    uint32_t* kslot = big_nk ? koff + 4 * gk_stride : s_kslot;
     for (int j = threadIdx.x; j < nk; j += kE2T) {
       const int64_t k = __ldg(A.col + a0 + j);
       uint32_t p0 = (uint32_t)B.rp(k), p1 = (uint32_t)B.rp(k + 1);
+      const int32_t sl = __ldg(bslot + k);
+      kslot[j] = (uint32_t)sl;
       if (!it.kind) {
-        const int32_t sl = __ldg(bslot + k);
         if (sl >= 0) {
           const uint32_t* ix = bidx + (size_t)sl * nwin1;
           p0 = __ldg(ix + min((int64_t)(clo >> ilog), nwin1 - 1));
@@ -499,11 +532,12 @@ k_bin_expand2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_
     }
     const int64_t rowbase = hbase[it.h] - batch_base;
     if (big_nk)
-      exp2_unit(B, (const uint32_t*)koff, (const uint32_t*)kpos, (const double*)kav, nk, T, shift,
-                (uint32_t)(rb.b0 + it.ja), cnt, e, it.ja, nent, bcol + rowbase, bval + rowbase, scratch);
+      exp2_unit(B, (const uint32_t*)koff, (const uint32_t*)kpos, (const double*)kav, (const uint32_t*)kslot, nk, T, shift,
+                (uint32_t)(rb.b0 + it.ja), cnt, e, it.ja, nent, bcol + rowbase, bval + rowbase, bidx, nwin1, scratch);
     else
-      exp2_unit(B, (const uint32_t*)s_koff, (const uint32_t*)s_kpos, (const double*)s_kav, nk, T, shift,
-                (uint32_t)(rb.b0 + it.ja), cnt, e, it.ja, nent, bcol + rowbase, bval + rowbase, scratch);
+      exp2_unit(B, (const uint32_t*)s_koff, (const uint32_t*)s_kpos, (const double*)s_kav, (const uint32_t*)s_kslot, nk, T,
+                shift, (uint32_t)(rb.b0 + it.ja), cnt, e, it.ja, nent, bcol + rowbase, bval + rowbase, bidx, nwin1,
+                scratch);
   }
 }
 

@@ -811,7 +811,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   occ_e2 = std::max(occ_e2, 1);
   uint32_t* e2scr = nullptr;   // per-CTA segment tables of units with more than kE2K k's
   const int64_t e2_stride = ((ctx->host_stats[mg::kStatMaxNk] + 8 + 3) / 4) * 4;
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&e2scr), (size_t)ctx->sm_count * occ_e2 * 4 * e2_stride * 4, s));
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&e2scr), (size_t)ctx->sm_count * occ_e2 * 5 * e2_stride * 4, s));
   std::vector<int64_t> hb(cuts.size());
   {
     int64_t a = 0;
