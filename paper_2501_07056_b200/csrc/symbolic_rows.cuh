@@ -38,7 +38,10 @@ constexpr int kS2Words = (1 << kS2WinLog) / 32;
 constexpr int kS2Touch = MG_S2_TOUCH;             // touched-word list (full scan of the row's words beyond it)
 constexpr int kS2Chunks = 2048;            // chunk counters per row
 constexpr int kS2K = MG_S2_K;                 // k's whose stream offsets live in shared memory
-constexpr int kS2U = 4;                    // waves of loads in flight per warp
+#ifndef MG_S2_U
+#define MG_S2_U 4
+#endif
+constexpr int kS2U = MG_S2_U;              // waves of loads in flight per warp
 
 struct Sym2Smem {
   static constexpr size_t kBitmap = (size_t)kS2Words * 4;
