@@ -121,6 +121,30 @@ int magnus_numeric_host(magnus_ctx* ctx, const int64_t* c_row_ptr, uint32_t* c_c
  * reducer), products and distinct columns in the other chunks (sort reducer).  Synchronises. */
 int magnus_heavy_stats(magnus_ctx* ctx, int64_t* out4);
 
+/* ---- Gustavson baselines (reference gustavson.py:155-268; the ablation without locality generation).
+ * Dense: one CTA per row over a full-width accumulator.  scratch (device) must hold at least
+ * magnus_gd_scratch_bytes(B->n_cols, 1) bytes; more lets more rows run concurrently (up to 4 per SM).
+ * gustavson_dense_symbolic (gustavson.py:155-170): c_row_ptr (n_rows+1, device) = exclusive prefix of the
+ * per-row distinct counts.  Synchronises. */
+size_t magnus_gd_scratch_bytes(int64_t n_cols, int64_t ctas);
+int magnus_gd_symbolic(const magnus_csr* A, const magnus_csr* B, int64_t* c_row_ptr, void* scratch, size_t scratch_bytes,
+                       void* stream);
+/* gustavson_dense_numeric (gustavson.py:184-220): values sequential from +0.0 in Gustavson order, rows
+ * emitted sorted (canonicalize_csr).  MAGNUS_CONTRACT if a row's count differs from c_row_ptr.  Synchronises. */
+int magnus_gd_numeric(const magnus_csr* A, const magnus_csr* B, const int64_t* c_row_ptr, uint32_t* c_col, double* c_val,
+                      void* scratch, size_t scratch_bytes, void* stream);
+/* gustavson_esc_numeric (gustavson.py:223-250), expand step: the products of rows [r0, r1) in Gustavson
+ * order; row r's start at inter_off[r] - inter_off[r0] (inter_off = exclusive prefix of the rows' product
+ * counts, device int64).  key = (r - r0) << 32 | col, val = B.val * A.val. */
+int magnus_esc_expand(const magnus_csr* A, const magnus_csr* B, int64_t r0, int64_t r1, const int64_t* inter_off,
+                      uint64_t* keys, double* vals, void* stream);
+/* compress step over keys sorted stably (perm: source index of each sorted key into vals): run j of
+ * equal keys -> C position out0 + j, column = key's low 32 bits, value = x0 + pairwise(x1..x_{d-1})
+ * (sort_accumulate accumulators.py:113-129).  run_scratch: n+1 int64.  *runs_out (host) = number of runs
+ * (synchronises before the reduce; with c_col or c_val NULL only the runs are counted). */
+int magnus_esc_compress(const uint64_t* keys, const int64_t* perm, const double* vals, int64_t n, int64_t out0,
+                        uint32_t* c_col, double* c_val, int64_t* run_scratch, int64_t* runs_out, void* stream);
+
 const char* magnus_last_error(void);
 const char* magnus_version(void);
 

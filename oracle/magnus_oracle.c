@@ -686,3 +686,54 @@ int oracle_setup(const oracle_csr* A, const oracle_csr* B, const oracle_sys* sys
 }
 
 double oracle_pairwise_sum(const double* a, int64_t n) { return pairwise_sum(a, n); }
+
+/* --------------------------------------------------------- Gustavson baselines */
+/* gustavson_dense_symbolic gustavson.py:155-170 (np.unique of the row's product),
+ * gustavson_dense_numeric gustavson.py:184-220 (DenseAccumulator over all n_cols:
+ * sequential from +0.0 in Gustavson order, then canonicalize_csr sorts the row),
+ * gustavson_esc_numeric gustavson.py:223-250 (sort_accumulate: x0 + pairwise(rest)).
+ * phase 0: row_ptr (n+1) out.  phase 1 (dense) / 2 (esc): col/val filled for row_ptr. */
+int oracle_gustavson(const oracle_csr* A, const oracle_csr* B, int phase, int threads, int64_t* row_ptr, uint32_t* c_col,
+                     double* c_val) {
+  if (A->n_cols != B->n_rows) return fail(ORACLE_INPUT, "dimension mismatch");
+  const int64_t n = A->n_rows;
+  if (phase && row_ptr[0] != 0) return fail(ORACLE_CONTRACT, "row_ptr does not come from a symbolic pass of (A, B)");
+  int64_t* counts = phase ? NULL : (int64_t*)calloc((size_t)(n + 1), sizeof(int64_t));
+  int err = 0;
+  if (threads > 0) omp_set_num_threads(threads);
+  #pragma omp parallel
+  {
+    scratch_t s;
+    memset(&s, 0, sizeof s);
+    int64_t cap = 0;
+    int64_t* cols = NULL; double* vals = NULL; int64_t* oc = NULL; double* ov = NULL;
+    #pragma omp for schedule(dynamic, 64)
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t m = 0;
+      for (int64_t t = A->row_ptr[i]; t < A->row_ptr[i + 1]; ++t) m += B->row_ptr[A->col[t] + 1] - B->row_ptr[A->col[t]];
+      if (m > cap) {
+        cap = m * 2 + 16;
+        cols = (int64_t*)realloc(cols, (size_t)cap * 8); vals = (double*)realloc(vals, (size_t)cap * 8);
+        oc = (int64_t*)realloc(oc, (size_t)cap * 8); ov = (double*)realloc(ov, (size_t)cap * 8);
+      }
+      gather_row(A, B, i, cols, phase ? vals : NULL);
+      int derr = 0;
+      int64_t got;
+      if (phase == 2) got = sort_accumulate(&s, cols, vals, m, oc, ov);
+      else got = dense_accumulate(&s, cols, phase ? vals : NULL, m, B->n_cols > 0 ? B->n_cols : 1, phase ? oc : NULL,
+                                  phase ? ov : NULL, &derr);
+      if (!phase) { counts[i] = got; continue; }
+      if (derr || got != row_ptr[i + 1] - row_ptr[i]) { _Pragma("omp atomic write") err = 1; continue; }
+      for (int64_t t = 0; t < got; ++t) { c_col[row_ptr[i] + t] = (uint32_t)oc[t]; c_val[row_ptr[i] + t] = ov[t]; }
+    }
+    free(cols); free(vals); free(oc); free(ov);
+    scratch_free(&s);
+  }
+  if (!phase) {
+    row_ptr[0] = 0;
+    for (int64_t i = 0; i < n; ++i) row_ptr[i + 1] = row_ptr[i] + counts[i];
+    free(counts);
+  }
+  if (err) return fail(ORACLE_CONTRACT, "numeric phase count differs from the symbolic count");
+  return ORACLE_OK;
+}

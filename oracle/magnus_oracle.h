@@ -27,6 +27,9 @@ int oracle_numeric(const oracle_csr* A, const oracle_csr* B, const oracle_sys* s
 int oracle_setup(const oracle_csr* A, const oracle_csr* B, const oracle_sys* sys, const oracle_thresholds* th,
                  int force_fine_only, int64_t* inter, int64_t* mn, int64_t* mx, int8_t* cat);
 double oracle_pairwise_sum(const double* a, int64_t n);
+/* Gustavson baselines (gustavson.py:155-250): phase 0 symbolic -> row_ptr; 1 dense numeric; 2 esc numeric */
+int oracle_gustavson(const oracle_csr* A, const oracle_csr* B, int phase, int threads, int64_t* row_ptr, uint32_t* c_col,
+                     double* c_val);
 const char* oracle_last_error(void);
 #ifdef __cplusplus
 }

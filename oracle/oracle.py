@@ -141,3 +141,23 @@ def spgemm(A, B, sys, thresholds=None, force_fine_only=False, threads=0) -> Orac
 def pairwise_sum(x: np.ndarray) -> float:
     x = np.ascontiguousarray(x, dtype=np.float64)
     return lib().oracle_pairwise_sum(x.ctypes.data, x.size)
+
+
+def gustavson(A, B, esc: bool = False, threads: int = 0) -> OracleResult:
+    """Reference gustavson_dense / gustavson_esc (gustavson.py:155-268) on the CPU."""
+    keep = []
+    a, b = _csr(A, keep), _csr(B, keep)
+    L = lib()
+    rp = np.empty(A.n_rows + 1, np.int64)
+    rc = L.oracle_gustavson(C.byref(a), C.byref(b), 0, int(threads), rp.ctypes.data_as(C.c_void_p), None, None)
+    if rc:
+        _raise(rc)
+    nnz = int(rp[-1])
+    col = np.empty(nnz, np.uint32)
+    val = np.empty(nnz, np.float64)
+    rc = L.oracle_gustavson(C.byref(a), C.byref(b), 2 if esc else 1, int(threads), rp.ctypes.data_as(C.c_void_p),
+                            col.ctypes.data_as(C.c_void_p), val.ctypes.data_as(C.c_void_p))
+    if rc:
+        _raise(rc)
+    inter = int(np.diff(np.asarray(B.row_ptr).astype(np.int64))[np.asarray(A.col).astype(np.int64)].sum())
+    return OracleResult(rp, col, val, {"inter_prod_size": inter, "nnz_c": nnz})

@@ -8,6 +8,7 @@ Public API (same names as the reference):
     bound_inputs_for (the paper's minimum-data-volume model) and the error classes.
 Device-only additions: detect_device_params, MagnusPlan (the two phases),
 parallel.spgemm_magnus_distributed (row-block split over ranks).
+Baselines (reference gustavson.py:155-268, on the device): gustavson_dense, gustavson_esc and their phases.
 """
 
 from .accumulators import Accum, AccumThresholds, merge_chunks_for_sort, select_accumulator
@@ -22,8 +23,13 @@ __all__ = [
     "OverBudgetError", "ParseError", "SpgemmError", "CsrMatrix", "RowStats", "validate_csr", "NUMERIC", "SYMBOLIC",
     "ChunkPlan", "SystemParams", "b200_default_params", "compute_chunk_plan", "detect_device_params", "with_overrides",
     "spgemm_magnus", "SpgemmResult", "RowCategories", "MagnusPlan", "row_intermediate_stats", "IdealBoundInputs",
-    "bound_inputs_for", "col_index_bytes", "ideal_bound",
+    "bound_inputs_for", "col_index_bytes", "ideal_bound", "gustavson_dense", "gustavson_esc", "gustavson_dense_symbolic",
+    "gustavson_dense_numeric", "gustavson_esc_numeric",
 ]
+
+
+_GUSTAVSON = ("gustavson_dense", "gustavson_esc", "gustavson_dense_symbolic", "gustavson_dense_numeric",
+              "gustavson_esc_numeric")
 
 
 def __getattr__(name):
@@ -32,4 +38,7 @@ def __getattr__(name):
     if name in ("spgemm_magnus", "SpgemmResult", "RowCategories", "MagnusPlan", "row_intermediate_stats"):
         from . import magnus
         return getattr(magnus, name)
+    if name in _GUSTAVSON:
+        from . import gustavson
+        return getattr(gustavson, name)
     raise AttributeError(name)

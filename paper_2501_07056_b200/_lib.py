@@ -73,7 +73,8 @@ class Counters(C.Structure):
 EXPORTS = ["magnus_compute_chunk_plan", "magnus_ctx_create", "magnus_ctx_destroy", "magnus_setup", "magnus_symbolic",
            "magnus_numeric", "magnus_row_stats", "magnus_categories", "magnus_launch_count", "magnus_last_error",
            "magnus_version", "magnus_profile_enable", "magnus_profile_read", "magnus_heavy_stats",
-           "magnus_numeric_host"]
+           "magnus_numeric_host", "magnus_gd_scratch_bytes", "magnus_gd_symbolic", "magnus_gd_numeric",
+           "magnus_esc_expand", "magnus_esc_compress"]
 KERNEL_NAMES = ["row_stats", "categorize", "sym_warp", "sym_block", "sym_heavy", "scan", "num_warp", "num_block",
                 "num_heavy", "sym_dense", "num_dense", "bin_plan", "bin_expand", "bin_reduce", "bin_big", "dir_index",
                 "dir_plan", "dir_num"]
@@ -111,6 +112,15 @@ def lib():
         L.magnus_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.magnus_heavy_stats.argtypes = [C.c_void_p, C.c_void_p]
         L.magnus_compute_chunk_plan.argtypes = [C.POINTER(Sys), C.c_int64, C.c_int, C.c_int, C.POINTER(Plan)]
+        L.magnus_gd_scratch_bytes.restype = C.c_size_t
+        L.magnus_gd_scratch_bytes.argtypes = [C.c_int64, C.c_int64]
+        L.magnus_gd_symbolic.argtypes = [C.POINTER(Csr), C.POINTER(Csr), C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+        L.magnus_gd_numeric.argtypes = [C.POINTER(Csr), C.POINTER(Csr), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_size_t, C.c_void_p]
+        L.magnus_esc_expand.argtypes = [C.POINTER(Csr), C.POINTER(Csr), C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]
+        L.magnus_esc_compress.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
         _LIB = L
     return _LIB
 

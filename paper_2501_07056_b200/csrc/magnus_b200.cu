@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "../../include/magnus_b200.h"
+#include "baselines.cuh"
 #include "binned_rows.cuh"
 #include "common.cuh"
 #include "dense_rows.cuh"
@@ -1120,6 +1121,128 @@ int magnus_debug_phases(unsigned long long* out16, int reset) {
   for (int i = 0; i < 16; ++i) out16[i] = 0;
   (void)reset;
 #endif
+  return MAGNUS_OK;
+}
+
+// ---------------------------------------------------------------- Gustavson baselines (gustavson.py:155-268)
+size_t magnus_gd_scratch_bytes(int64_t n_cols, int64_t ctas) {
+  const int64_t nwords = (std::max<int64_t>(n_cols, 1) + 31) / 32;
+  return (size_t)ctas * (size_t)nwords * (4 + 32 * 8);
+}
+
+static int gd_launch(const magnus_csr* A, const magnus_csr* B, int numeric, const int64_t* c_rp, int64_t* rp_out,
+                     uint32_t* c_col, double* c_val, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  if (!A || !B || (!scratch && A->n_rows)) return set_err(MAGNUS_INPUT, "null argument");
+  if (A->n_cols != B->n_rows)
+    return set_err(MAGNUS_INPUT, "dimension mismatch: A is " + std::to_string(A->n_rows) + "x" + std::to_string(A->n_cols) +
+                                     ", B is " + std::to_string(B->n_rows) + "x" + std::to_string(B->n_cols));
+  if (B->n_cols > (int64_t(1) << 32)) return set_err(MAGNUS_INPUT, "more than 2^32 columns needs 8-byte column indices");
+  const int64_t n = A->n_rows;
+  if (n == 0) {
+    if (!numeric) MG_CUDA(cudaMemsetAsync(rp_out, 0, 8, s));
+    return MAGNUS_OK;
+  }
+  int dev = 0, sms = 148;
+  MG_CUDA(cudaGetDevice(&dev));
+  MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t nwords = (std::max<int64_t>(B->n_cols, 1) + 31) / 32;
+  const size_t per = magnus_gd_scratch_bytes(B->n_cols, 1);
+  const int64_t ctas = std::min<int64_t>({(int64_t)sms * 4, (int64_t)(scratch_bytes / per), n});
+  if (ctas < 1)
+    return set_err(MAGNUS_OVER_BUDGET, "scratch of " + std::to_string(scratch_bytes) + " bytes holds no " +
+                                           std::to_string(per) + "-byte dense accumulator");
+  uint32_t* bm = static_cast<uint32_t*>(scratch);
+  double* acc = reinterpret_cast<double*>(bm + (size_t)ctas * nwords + ((size_t)ctas * nwords & 1));
+  unsigned long long* flags = nullptr;
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), 16, s));
+  MG_CUDA(cudaMemsetAsync(flags, 0, 16, s));
+  MG_CUDA(cudaMemsetAsync(bm, 0, (size_t)ctas * nwords * 4, s));
+  const mg::DevCsr dA = dev_csr(*A), dB = dev_csr(*B);
+  if (numeric)
+    mg::k_gd_rows<true><<<(unsigned)ctas, mg::kGdT, 0, s>>>(dA, dB, c_rp, c_col, c_val, nullptr, bm, acc, nwords, flags,
+                                                            flags + 1);
+  else
+    mg::k_gd_rows<false><<<(unsigned)ctas, mg::kGdT, 0, s>>>(dA, dB, nullptr, nullptr, nullptr, rp_out, bm, nullptr,
+                                                             nwords, flags, flags + 1);
+  MG_CUDA(cudaGetLastError());
+  unsigned long long err = 0;
+  if (!numeric) {
+    // row_ptr = exclusive scan of the per-row counts, in place (k_scan_apply reads and writes each index
+    // from the same thread)
+    const int64_t tiles = (n + mg::kScanTile - 1) / mg::kScanTile;
+    int64_t* tile_sums = nullptr;
+    MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tile_sums), (size_t)(tiles + 1) * 8, s));
+    mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(rp_out, n, tile_sums);
+    mg::k_scan_tiles<<<1, 1024, 0, s>>>(tile_sums, tiles);
+    mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(rp_out, n, tile_sums, rp_out);
+    MG_CUDA(cudaGetLastError());
+    MG_CUDA(cudaFreeAsync(tile_sums, s));
+  } else {
+    MG_CUDA(cudaMemcpyAsync(&err, flags + 1, 8, cudaMemcpyDeviceToHost, s));
+  }
+  MG_CUDA(cudaFreeAsync(flags, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  if (err) return set_err(MAGNUS_CONTRACT, "numeric phase count differs from the symbolic count");
+  return MAGNUS_OK;
+}
+
+int magnus_gd_symbolic(const magnus_csr* A, const magnus_csr* B, int64_t* c_row_ptr, void* scratch, size_t scratch_bytes,
+                       void* stream) {
+  if (!c_row_ptr) return set_err(MAGNUS_INPUT, "null argument");
+  return gd_launch(A, B, 0, nullptr, c_row_ptr, nullptr, nullptr, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+int magnus_gd_numeric(const magnus_csr* A, const magnus_csr* B, const int64_t* c_row_ptr, uint32_t* c_col, double* c_val,
+                      void* scratch, size_t scratch_bytes, void* stream) {
+  if (!c_row_ptr) return set_err(MAGNUS_INPUT, "null argument");
+  return gd_launch(A, B, 1, c_row_ptr, nullptr, c_col, c_val, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+int magnus_esc_expand(const magnus_csr* A, const magnus_csr* B, int64_t r0, int64_t r1, const int64_t* inter_off,
+                      uint64_t* keys, double* vals, void* stream) {
+  if (!A || !B || !inter_off) return set_err(MAGNUS_INPUT, "null argument");
+  if (A->n_cols != B->n_rows) return set_err(MAGNUS_INPUT, "dimension mismatch");
+  if (r0 < 0 || r1 > A->n_rows || r0 > r1) return set_err(MAGNUS_INPUT, "row range outside A");
+  if (r1 - r0 > (int64_t(1) << 31)) return set_err(MAGNUS_INPUT, "row range wider than 2^31");
+  if (r1 == r0) return MAGNUS_OK;
+  int dev = 0, sms = 148;
+  MG_CUDA(cudaGetDevice(&dev));
+  MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t blocks = std::min<int64_t>((r1 - r0 + 7) / 8, (int64_t)sms * 8);
+  mg::k_esc_expand<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(dev_csr(*A), dev_csr(*B), r0, r1, inter_off, keys,
+                                                                       vals);
+  MG_CUDA(cudaGetLastError());
+  return MAGNUS_OK;
+}
+
+int magnus_esc_compress(const uint64_t* keys, const int64_t* perm, const double* vals, int64_t n, int64_t out0,
+                        uint32_t* c_col, double* c_val, int64_t* run_scratch, int64_t* runs_out, void* stream) {
+  if (n < 0 || (n && (!keys || !perm || !vals || !run_scratch))) return set_err(MAGNUS_INPUT, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) {
+    if (runs_out) *runs_out = 0;
+    return MAGNUS_OK;
+  }
+  int dev = 0, sms = 148;
+  MG_CUDA(cudaGetDevice(&dev));
+  MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16);
+  mg::k_esc_heads<<<g, 256, 0, s>>>(keys, n, run_scratch);
+  const int64_t tiles = (n + mg::kScanTile - 1) / mg::kScanTile;
+  int64_t* tile_sums = nullptr;
+  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tile_sums), (size_t)(tiles + 1) * 8, s));
+  mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(run_scratch, n, tile_sums);
+  mg::k_scan_tiles<<<1, 1024, 0, s>>>(tile_sums, tiles);
+  mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(run_scratch, n, tile_sums, run_scratch);
+  MG_CUDA(cudaFreeAsync(tile_sums, s));
+  int64_t runs = 0;
+  MG_CUDA(cudaMemcpyAsync(&runs, run_scratch + n, 8, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  if (runs_out) *runs_out = runs;
+  if (c_col && c_val) {
+    mg::k_esc_reduce<<<g, 256, 0, s>>>(keys, perm, vals, n, run_scratch, out0, c_col, c_val);
+    MG_CUDA(cudaGetLastError());
+  }
   return MAGNUS_OK;
 }
 
