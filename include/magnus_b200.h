@@ -145,6 +145,26 @@ int magnus_esc_expand(const magnus_csr* A, const magnus_csr* B, int64_t r0, int6
 int magnus_esc_compress(const uint64_t* keys, const int64_t* perm, const double* vals, int64_t n, int64_t out0,
                         uint32_t* c_col, double* c_val, int64_t* run_scratch, int64_t* runs_out, void* stream);
 
+/* ---- building-block microbenchmarks (reference bench.py:88-196): one synthetic stream of u32
+ * indices < length and f64 values, each stage a kernel of its own.  Device pointers; asynchronous.
+ * histogram: counts[c] = #{i : idx[i] >> shift == c} (int64, n_chunks <= 16384). */
+int magnus_mb_histogram(const uint32_t* idx, int64_t n, int shift, int n_chunks, int64_t* counts, void* stream);
+/* reorder: stable scatter of (idx & (2^shift - 1), val) into chunk order (stable_scatter_positions
+ * matrix.py:187-204); n_chunks <= 4096; scratch of magnus_mb_reorder_scratch_bytes(n, n_chunks). */
+size_t magnus_mb_reorder_scratch_bytes(int64_t n, int n_chunks);
+int magnus_mb_reorder(const uint32_t* idx, const double* val, int64_t n, int shift, int n_chunks, void* scratch,
+                      size_t scratch_bytes, uint32_t* out_col, double* out_val, void* stream);
+/* dense accumulation per chunk (dense_accumulate accumulators.py:68-97; sequential from +0.0 in slice
+ * order): chunk c's slice [offsets[c], offsets[c+1]) of chunk-local columns < chunk_len (<= 16384) is
+ * replaced at its start by its distinct columns ascending and their sums; distinct[c] = their number. */
+int magnus_mb_dense(const uint32_t* col, const double* val, const int64_t* offsets, int n_chunks, int chunk_len,
+                    uint32_t* out_col, double* out_val, int64_t* distinct, void* stream);
+/* exclusive prefix sum: out[0..n] (out[n] = total) of int64 in[0..n); scratch of magnus_mb_scan_scratch_bytes(n). */
+size_t magnus_mb_scan_scratch_bytes(int64_t n);
+int magnus_mb_scan(const int64_t* in, int64_t n, int64_t* out, void* scratch, void* stream);
+/* contiguous copy (the streaming baseline): bytes (multiple of 16, 16-byte aligned). */
+int magnus_mb_stream(const void* src, void* dst, int64_t bytes, void* stream);
+
 const char* magnus_last_error(void);
 const char* magnus_version(void);
 

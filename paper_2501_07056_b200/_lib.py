@@ -74,7 +74,9 @@ EXPORTS = ["magnus_compute_chunk_plan", "magnus_ctx_create", "magnus_ctx_destroy
            "magnus_numeric", "magnus_row_stats", "magnus_categories", "magnus_launch_count", "magnus_last_error",
            "magnus_version", "magnus_profile_enable", "magnus_profile_read", "magnus_heavy_stats",
            "magnus_numeric_host", "magnus_gd_scratch_bytes", "magnus_gd_symbolic", "magnus_gd_numeric",
-           "magnus_esc_expand", "magnus_esc_compress"]
+           "magnus_esc_expand", "magnus_esc_compress", "magnus_mb_histogram", "magnus_mb_reorder_scratch_bytes",
+           "magnus_mb_reorder", "magnus_mb_dense", "magnus_mb_stream",
+           "magnus_mb_scan_scratch_bytes", "magnus_mb_scan"]
 KERNEL_NAMES = ["row_stats", "categorize", "sym_warp", "sym_block", "sym_heavy", "scan", "num_warp", "num_block",
                 "num_heavy", "sym_dense", "num_dense", "bin_plan", "bin_expand", "bin_reduce", "bin_big", "dir_index",
                 "dir_plan", "dir_num"]
@@ -121,6 +123,17 @@ def lib():
                                         C.c_void_p, C.c_void_p]
         L.magnus_esc_compress.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
                                           C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p]
+        L.magnus_mb_histogram.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.magnus_mb_reorder_scratch_bytes.restype = C.c_size_t
+        L.magnus_mb_reorder_scratch_bytes.argtypes = [C.c_int64, C.c_int]
+        L.magnus_mb_reorder.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p, C.c_size_t,
+                                        C.c_void_p, C.c_void_p, C.c_void_p]
+        L.magnus_mb_dense.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p]
+        L.magnus_mb_scan_scratch_bytes.restype = C.c_size_t
+        L.magnus_mb_scan_scratch_bytes.argtypes = [C.c_int64]
+        L.magnus_mb_scan.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.magnus_mb_stream.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         _LIB = L
     return _LIB
 

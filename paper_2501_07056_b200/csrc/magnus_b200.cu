@@ -17,6 +17,7 @@
 #include "../../include/magnus_b200.h"
 #include "baselines.cuh"
 #include "binned_rows.cuh"
+#include "microbench.cuh"
 #include "common.cuh"
 #include "dense_rows.cuh"
 #include "direct_rows.cuh"
@@ -1243,6 +1244,98 @@ int magnus_esc_compress(const uint64_t* keys, const int64_t* perm, const double*
     mg::k_esc_reduce<<<g, 256, 0, s>>>(keys, perm, vals, n, run_scratch, out0, c_col, c_val);
     MG_CUDA(cudaGetLastError());
   }
+  return MAGNUS_OK;
+}
+
+// ---------------------------------------------------------------- building-block microbenchmarks (bench.py:88-196)
+static int sm_count() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+int magnus_mb_histogram(const uint32_t* idx, int64_t n, int shift, int n_chunks, int64_t* counts, void* stream) {
+  if (n_chunks < 1 || n_chunks > 16384 || shift < 0 || shift > 31 || (n && !idx) || !counts)
+    return set_err(MAGNUS_INPUT, "histogram: 1 <= n_chunks <= 16384, 0 <= shift < 32");
+  cudaStream_t s = (cudaStream_t)stream;
+  MG_CUDA(cudaMemsetAsync(counts, 0, (size_t)n_chunks * 8, s));
+  if (!n) return MAGNUS_OK;
+  const int64_t g = std::min<int64_t>((n + 1023) / 1024, (int64_t)sm_count() * 4);
+  mg::k_mb_hist<<<(unsigned)g, 512, (size_t)n_chunks * 4, s>>>(idx, n, shift, n_chunks,
+                                                               reinterpret_cast<unsigned long long*>(counts));
+  MG_CUDA(cudaGetLastError());
+  return MAGNUS_OK;
+}
+
+size_t magnus_mb_reorder_scratch_bytes(int64_t n, int n_chunks) {
+  const int64_t ntiles = (n + mg::kMbTile - 1) / mg::kMbTile;
+  const int64_t tiles = (n_chunks * ntiles + mg::kScanTile - 1) / mg::kScanTile;
+  return (size_t)(n_chunks * ntiles + 1 + tiles + 1) * 8;
+}
+
+int magnus_mb_reorder(const uint32_t* idx, const double* val, int64_t n, int shift, int n_chunks, void* scratch,
+                      size_t scratch_bytes, uint32_t* out_col, double* out_val, void* stream) {
+  if (n_chunks < 1 || n_chunks > mg::kMbMaxChunks || shift < 0 || shift > 31)
+    return set_err(MAGNUS_INPUT, "reorder: 1 <= n_chunks <= 4096, 0 <= shift < 32");
+  if (n >= (int64_t(1) << 32)) return set_err(MAGNUS_INPUT, "reorder: stream longer than 2^32");
+  if (scratch_bytes < magnus_mb_reorder_scratch_bytes(n, n_chunks)) return set_err(MAGNUS_INPUT, "reorder: scratch too small");
+  if (!n) return MAGNUS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t ntiles = (n + mg::kMbTile - 1) / mg::kMbTile, m = (int64_t)n_chunks * ntiles;
+  int64_t* toff = static_cast<int64_t*>(scratch);
+  int64_t* tile_sums = toff + m + 1;
+  const size_t sh = (size_t)mg::kMbWarps * n_chunks * 4;
+  MG_CUDA(cudaFuncSetAttribute(mg::k_mb_tile_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_mb_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+  const unsigned g = (unsigned)((ntiles + mg::kMbWarps - 1) / mg::kMbWarps);
+  mg::k_mb_tile_hist<<<g, mg::kMbWarps * 32, sh, s>>>(idx, n, shift, n_chunks, ntiles, toff);
+  const int64_t tiles = (m + mg::kScanTile - 1) / mg::kScanTile;
+  mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(toff, m, tile_sums);
+  mg::k_scan_tiles<<<1, 1024, 0, s>>>(tile_sums, tiles);
+  mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(toff, m, tile_sums, toff);
+  mg::k_mb_scatter<<<g, mg::kMbWarps * 32, sh, s>>>(idx, val, n, shift, n_chunks, ntiles, toff, out_col, out_val);
+  MG_CUDA(cudaGetLastError());
+  return MAGNUS_OK;
+}
+
+int magnus_mb_dense(const uint32_t* col, const double* val, const int64_t* offsets, int n_chunks, int chunk_len,
+                    uint32_t* out_col, double* out_val, int64_t* distinct, void* stream) {
+  if (n_chunks < 1 || chunk_len < 1 || chunk_len > (1 << 14)) return set_err(MAGNUS_INPUT, "dense: 1 <= chunk_len <= 16384");
+  const size_t sh = (size_t)chunk_len * 8 + (size_t)((chunk_len + 63) / 64) * 8 + 32 * 8;
+  MG_CUDA(cudaFuncSetAttribute(mg::k_mb_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
+  mg::k_mb_dense<<<(unsigned)n_chunks, 32, sh, (cudaStream_t)stream>>>(col, val, offsets, n_chunks, chunk_len, out_col,
+                                                                       out_val, distinct);
+  MG_CUDA(cudaGetLastError());
+  return MAGNUS_OK;
+}
+
+size_t magnus_mb_scan_scratch_bytes(int64_t n) { return (size_t)((n + mg::kScanTile - 1) / mg::kScanTile + 1) * 8; }
+
+int magnus_mb_scan(const int64_t* in, int64_t n, int64_t* out, void* scratch, void* stream) {
+  if (n < 0 || !out || (n && (!in || !scratch))) return set_err(MAGNUS_INPUT, "scan: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!n) {
+    MG_CUDA(cudaMemsetAsync(out, 0, 8, s));
+    return MAGNUS_OK;
+  }
+  const int64_t tiles = (n + mg::kScanTile - 1) / mg::kScanTile;
+  int64_t* tile_sums = static_cast<int64_t*>(scratch);
+  mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(in, n, tile_sums);
+  mg::k_scan_tiles<<<1, 1024, 0, s>>>(tile_sums, tiles);
+  mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(in, n, tile_sums, out);
+  MG_CUDA(cudaGetLastError());
+  return MAGNUS_OK;
+}
+
+int magnus_mb_stream(const void* src, void* dst, int64_t bytes, void* stream) {
+  if (bytes < 0 || (bytes & 15) || (((uintptr_t)src | (uintptr_t)dst) & 15))
+    return set_err(MAGNUS_INPUT, "stream: 16-byte aligned buffers and sizes");
+  if (!bytes) return MAGNUS_OK;
+  const int64_t n16 = bytes / 16;
+  const unsigned g = (unsigned)std::min<int64_t>((n16 + 255) / 256, (int64_t)sm_count() * 8);
+  mg::k_mb_stream<<<g, 256, 0, (cudaStream_t)stream>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst), n16);
+  MG_CUDA(cudaGetLastError());
   return MAGNUS_OK;
 }
 
