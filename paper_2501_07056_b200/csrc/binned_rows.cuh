@@ -318,7 +318,20 @@ struct E2Cursor {
     seg = kk;
     if (q0 + 31 < kend || q0 >= q_end) return false;
     int kl = kk;
-    while (kl < nk && koff[kl + 1] <= q) ++kl;
+#ifndef MG_E2_SCAN_SEG
+    // lane j holds the start of segment kk+1+j; when the wave ends before the 32nd of them, a
+    // lane's segment is kk + (starts <= q), found by a 5-step search over the shuffled starts
+    const int jb = kk + 1 + (threadIdx.x & 31);
+    const uint32_t bnd = jb <= nk ? koff[jb] : 0xffffffffu;
+    if (__shfl_sync(0xffffffffu, bnd, 31) > q0 + 31) {
+      int cnt = 0;
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1)
+        if (__shfl_sync(0xffffffffu, bnd, cnt + st - 1) <= q) cnt += st;
+      kl += cnt;
+    } else
+#endif
+      while (kl < nk && koff[kl + 1] <= q) ++kl;
     pos = kpos[kl] + (q - koff[kl]);
     seg = kl;
     kk = __shfl_sync(0xffffffffu, kl, 31);
@@ -464,6 +477,8 @@ __device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA 
   (void)scratch;
 }
 
+// (no minBlocks argument: an explicit 1 lets ptxas take 78 registers, 3 CTAs/SM, 590 vs 543 ms per cfg3 step;
+// the default heuristic settles at 48 registers, 5 CTAs/SM)
 __global__ void __launch_bounds__(kE2T)
 k_bin_expand2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t* __restrict__ mn,
               const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce,
