@@ -339,6 +339,56 @@ struct E2Cursor {
     base = kpos[kk] - koff[kk];
     return true;
   }
+  // the kE2U waves from q00 at once (warp-uniform call, q00 < q_end): per wave the lane's B
+  // position, its segment and whether the wave may span several segments.  When the batch
+  // ends before the 32nd segment start after kk, every wave searches the same shuffled starts
+  // (one shared-memory load per batch, no cursor chain from wave to wave).
+  __device__ __forceinline__ void batch(uint32_t q00, uint32_t q_end, uint32_t (&pos)[kE2U], int (&seg)[kE2U],
+                                        bool (&multi)[kE2U]) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t qlast = q00 + 32 * kE2U - 1;
+    if (qlast < kend) {
+#pragma unroll
+      for (int u = 0; u < kE2U; ++u) {
+        pos[u] = base + q00 + 32 * u + lane;
+        seg[u] = kk;
+        multi[u] = false;
+      }
+      return;
+    }
+    const int jb = kk + 1 + (int)lane;
+    const uint32_t bnd = jb <= nk ? koff[jb] : 0xffffffffu;
+    const uint32_t qstop = min(qlast, q_end - 1);
+    if (__shfl_sync(0xffffffffu, bnd, 31) > qstop) {
+      auto starts_le = [&](uint32_t q) {
+        int cnt = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1)
+          if (__shfl_sync(0xffffffffu, bnd, cnt + st - 1) <= q) cnt += st;
+        return cnt;
+      };
+#pragma unroll
+      for (int u = 0; u < kE2U; ++u) {
+        const uint32_t q0 = q00 + 32 * u, q = q0 + lane;
+        if (q0 + 31 < kend) {
+          pos[u] = base + q;
+          seg[u] = kk;
+          multi[u] = false;
+        } else {
+          const int kl = kk + starts_le(min(q, qstop));
+          pos[u] = kpos[kl] + (q - koff[kl]);
+          seg[u] = kl;
+          multi[u] = true;
+        }
+      }
+      kk += starts_le(qstop);
+      kend = koff[kk + 1];
+      base = kpos[kk] - koff[kk];
+      return;
+    }
+#pragma unroll
+    for (int u = 0; u < kE2U; ++u) multi[u] = wave(q00 + 32 * u, q00 + 32 * u + lane, q_end, pos[u], seg[u]);
+  }
 };
 
 template <class KP, class KA, class KS>
@@ -361,14 +411,19 @@ __device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA 
     E2Cursor<KP> cur{koff, kpos, nk, 0, 0, 0};
     cur.init(qa);
     for (uint32_t q00 = qa; q00 < qb; q00 += 32 * kE2U) {
-      uint32_t cw[kE2U];
+      uint32_t cw[kE2U], pos[kE2U];
+      int seg[kE2U];
+      bool multi[kE2U];
+#ifdef MG_E2_WAVE_CURSOR
+#pragma unroll
+      for (int u = 0; u < kE2U; ++u) cur.wave(q00 + 32 * u, q00 + 32 * u + lane, qb, pos[u], seg[u]);
+#else
+      cur.batch(q00, qb, pos, seg, multi);
+#endif
 #pragma unroll
       for (int u = 0; u < kE2U; ++u) {
-        const uint32_t q0 = q00 + 32 * u, q = q0 + lane;
-        uint32_t pos;
-        int seg;
-        cur.wave(q0, q, qb, pos, seg);
-        cw[u] = q < qb ? __ldg(B.col + pos) : 0xffffffffu;
+        const uint32_t q = q00 + 32 * u + lane;
+        cw[u] = q < qb ? __ldg(B.col + pos[u]) : 0xffffffffu;
       }
 #pragma unroll
       for (int u = 0; u < kE2U; ++u) {
@@ -422,27 +477,44 @@ __device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA 
     }
   }
   __syncthreads();
-  // ---- pass 2: append (chunk-local column, product) to the slices
+  // ---- pass 2: append (chunk-local column, product) to the slices.  Software-pipelined: the B
+  // loads of the next batch of waves are issued before the current batch is ranked and stored.
   if (q_beg < q_end) {
     E2Cursor<KP> cur{koff, kpos, nk, 0, 0, 0};
     cur.init(q_beg);
+    uint32_t ncw[kE2U], pos[kE2U];
+    double nvv[kE2U];
+    bool nmulti[kE2U];
+    int nseg[kE2U];
+    auto fetch = [&](uint32_t q00) {
+      cur.batch(q00, q_end, pos, nseg, nmulti);
+#pragma unroll
+      for (int u = 0; u < kE2U; ++u) {
+        const uint32_t q = q00 + 32 * u + lane;
+        ncw[u] = 0xffffffffu;
+        nvv[u] = 0.0;
+        if (q < q_end) {
+          ncw[u] = __ldg(B.col + pos[u]);
+          nvv[u] = __ldg(B.val + pos[u]);
+        }
+      }
+    };
+    fetch(q_beg);
     for (uint32_t q00 = q_beg; q00 < q_end; q00 += 32 * kE2U) {
       uint32_t cw[kE2U];
       double vw[kE2U];
       bool multi[kE2U];
+      int seg[kE2U];
 #pragma unroll
       for (int u = 0; u < kE2U; ++u) {
-        const uint32_t q0 = q00 + 32 * u, q = q0 + lane;
-        uint32_t pos;
-        int seg;
-        multi[u] = cur.wave(q0, q, q_end, pos, seg);
-        cw[u] = 0xffffffffu;
-        vw[u] = 0.0;
-        if (q < q_end) {
-          cw[u] = __ldg(B.col + pos);
-          vw[u] = __dmul_rn(kav[seg], __ldg(B.val + pos));
-        }
+        cw[u] = ncw[u];
+        vw[u] = nvv[u];
+        multi[u] = nmulti[u];
+        seg[u] = nseg[u];
       }
+      if (q00 + 32 * kE2U < q_end) fetch(q00 + 32 * kE2U);
+#pragma unroll
+      for (int u = 0; u < kE2U; ++u) vw[u] = __dmul_rn(kav[seg[u]], vw[u]);
 #pragma unroll
       for (int u = 0; u < kE2U; ++u) {
         if (q00 + 32 * u >= q_end) break;
@@ -477,9 +549,12 @@ __device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA 
   (void)scratch;
 }
 
-// (no minBlocks argument: an explicit 1 lets ptxas take 78 registers, 3 CTAs/SM, 590 vs 543 ms per cfg3 step;
-// the default heuristic settles at 48 registers, 5 CTAs/SM)
-__global__ void __launch_bounds__(kE2T)
+// 4 CTAs/SM: the pipelined pass 2 fits 61 registers without spills (5 CTAs spill, 208 vs 162 ms on cfg3;
+// no minBlocks at all lets ptxas take 64 registers plus a stack)
+#ifndef MG_E2_MINB
+#define MG_E2_MINB 4
+#endif
+__global__ void __launch_bounds__(kE2T, MG_E2_MINB)
 k_bin_expand2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_t* __restrict__ mn,
               const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce,
               const int64_t* __restrict__ hbase, int64_t batch_base, const BinItem* __restrict__ units,
