@@ -343,13 +343,13 @@ struct E2Cursor {
   // position, its segment and whether the wave may span several segments.  When the batch
   // ends before the 32nd segment start after kk, every wave searches the same shuffled starts
   // (one shared-memory load per batch, no cursor chain from wave to wave).
-  __device__ __forceinline__ void batch(uint32_t q00, uint32_t q_end, uint32_t (&pos)[kE2U], int (&seg)[kE2U],
-                                        bool (&multi)[kE2U]) {
+  template <int U>
+  __device__ __forceinline__ void batch(uint32_t q00, uint32_t q_end, uint32_t (&pos)[U], int (&seg)[U], bool (&multi)[U]) {
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t qlast = q00 + 32 * kE2U - 1;
+    const uint32_t qlast = q00 + 32 * U - 1;
     if (qlast < kend) {
 #pragma unroll
-      for (int u = 0; u < kE2U; ++u) {
+      for (int u = 0; u < U; ++u) {
         pos[u] = base + q00 + 32 * u + lane;
         seg[u] = kk;
         multi[u] = false;

@@ -102,6 +102,7 @@ __device__ __forceinline__ void sym2_stream(const DevCsr& B, KP koff, KP kpos, i
   const uint32_t a_bm = (uint32_t)__cvta_generic_to_shared(bm), a_touch = (uint32_t)__cvta_generic_to_shared(touch),
                  a_nt = (uint32_t)__cvta_generic_to_shared(ntouch), a_cc = (uint32_t)__cvta_generic_to_shared(ccnt);
   const uint32_t lt = lanemask_lt(), le = lanemask_le();
+#ifdef MG_S2_WAVE_CURSOR
   // segment of the first position: last j with koff[j] <= q_beg
   int kk = 0;
   {
@@ -131,6 +132,30 @@ __device__ __forceinline__ void sym2_stream(const DevCsr& B, KP koff, KP kpos, i
       }
       cw[u] = q < q_end ? __ldg(B.col + pos) : 0xffffffffu;
     }
+#else
+  // batched segment cursor (E2Cursor::batch) and software pipelining: the column loads of the
+  // next kS2U waves are in flight while the current ones update the bitmap
+  E2Cursor<KP> cur{koff, kpos, nk, 0, 0, 0};
+  cur.init(q_beg);
+  uint32_t ncw[kS2U];
+  auto fetch = [&](uint32_t q00) {
+    uint32_t pos[kS2U];
+    int seg[kS2U];
+    bool multi[kS2U];
+    cur.batch(q00, q_end, pos, seg, multi);
+#pragma unroll
+    for (int u = 0; u < kS2U; ++u) {
+      const uint32_t q = q00 + 32 * u + lane;
+      ncw[u] = q < q_end ? __ldg(B.col + pos[u]) : 0xffffffffu;
+    }
+  };
+  fetch(q_beg);
+  for (uint32_t q00 = q_beg; q00 < q_end; q00 += 32 * kS2U) {
+    uint32_t cw[kS2U];
+#pragma unroll
+    for (int u = 0; u < kS2U; ++u) cw[u] = ncw[u];
+    if (q00 + 32 * kS2U < q_end) fetch(q00 + 32 * kS2U);
+#endif
 #pragma unroll
     for (int u = 0; u < kS2U; ++u) {
       if (q00 + 32 * u >= q_end) break;
