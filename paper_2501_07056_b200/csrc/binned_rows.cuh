@@ -1006,9 +1006,11 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
 // bytes per warp are in flight without registers.  Chunks above kBigSplit
 // elements are split into column parts handled by different warps.
 #ifndef MG_BIG_RS
-#define MG_BIG_RS 3
+#define MG_BIG_RS 33
 #endif
-constexpr int kBigRunSer = MG_BIG_RS;      // waves with fewer run breaks are applied run by run
+// waves with fewer run breaks are applied run by run, the others by match_any peer groups; 33 =
+// always run by run (match_any costs more than up to 32 predicated passes: 144 -> 124 ms on cfg3)
+constexpr int kBigRunSer = MG_BIG_RS;
 #ifndef MG_BIG_NS
 #define MG_BIG_NS 2
 #endif
