@@ -777,13 +777,14 @@ __device__ __forceinline__ bool reduce_chunk_sort(const uint16_t* sc, const doub
 // columns summed with the chunk's association -- sequential from +0.0 (dense) or
 // x0 + (((-0.0 + x1) + x2) + ...) (np.add.reduceat, numpy pairwise below 8 terms).
 // Returns 1 ok, 0 count mismatch.
-__device__ __forceinline__ int reduce_chunk_wave(const uint16_t* __restrict__ sc, const double* __restrict__ sv, uint32_t n,
-                                                 uint32_t m, bool seq, uint32_t colbase, uint32_t* __restrict__ c_col,
-                                                 double* __restrict__ c_val, int64_t out) {
+// (core: this lane's product already loaded -- cl its chunk-local column, v its value)
+__device__ __forceinline__ int reduce_chunk_wave_core(uint32_t cl, double v, uint32_t n, uint32_t m, bool seq,
+                                                      uint32_t colbase, uint32_t* __restrict__ c_col,
+                                                      double* __restrict__ c_val, int64_t out) {
   const int lane = threadIdx.x & 31;
   const bool valid = (uint32_t)lane < n;
-  uint32_t key = valid ? ((uint32_t)__ldg(sc + lane) << 5) | (uint32_t)lane : 0xffffffffu;
-  double v = valid ? __ldg(sv + lane) : 0.0;
+  uint32_t key = valid ? (cl << 5) | (uint32_t)lane : 0xffffffffu;
+  if (!valid) v = 0.0;
 #pragma unroll
   for (int k = 2; k <= 32; k <<= 1) {
 #pragma unroll
@@ -860,6 +861,15 @@ __device__ __forceinline__ int reduce_chunk_wave(const uint16_t* __restrict__ sc
   return __popc(hm) == m ? 1 : 0;
 }
 
+__device__ __forceinline__ int reduce_chunk_wave(const uint16_t* __restrict__ sc, const double* __restrict__ sv, uint32_t n,
+                                                 uint32_t m, bool seq, uint32_t colbase, uint32_t* __restrict__ c_col,
+                                                 double* __restrict__ c_val, int64_t out) {
+  const int lane = threadIdx.x & 31;
+  const bool valid = (uint32_t)lane < n;
+  return reduce_chunk_wave_core(valid ? (uint32_t)__ldg(sc + lane) : 0u, valid ? __ldg(sv + lane) : 0.0, n, m, seq, colbase,
+                                c_col, c_val, out);
+}
+
 // Prefetch the reorder-buffer range [q0, q1) of a window (columns + values) into L2: the
 // window's chunks are then reduced from L2 instead of one DRAM round trip each.
 __device__ __forceinline__ void prefetch_slice(const uint16_t* bcol, const double* bval, int64_t q0, int64_t q1) {
@@ -906,16 +916,31 @@ k_bin_reduce_tiny(const int32_t* __restrict__ rows, const int8_t* __restrict__ c
       const uint32_t d_l = j0 + lane <= it.jb ? __ldg(d + j0 + lane) : 0u;
       const int jn = min(it.jb - j0, 32);
       const uint32_t e_last = __ldg(e + j0 + jn), d_last = __ldg(d + j0 + jn);
-      for (int t = 0; t < jn; ++t) {
-        const uint32_t ej = __shfl_sync(0xffffffffu, e_l, t);
+      // software-pipelined: the next chunk's product is loaded while this one is sorted and summed
+      auto bounds = [&](int t, uint32_t& ej, uint32_t& n) {
+        ej = __shfl_sync(0xffffffffu, e_l, min(t, 31));
         const uint32_t en = t + 1 < 32 ? __shfl_sync(0xffffffffu, e_l, min(t + 1, 31)) : e_last;
+        n = (t + 1 == jn ? e_last : en) - ej;
+      };
+      uint32_t ej, n;
+      bounds(0, ej, n);
+      uint32_t ncl = (uint32_t)lane < n ? (uint32_t)__ldg(bcol + rowbase + ej + lane) : 0u;
+      double nv = (uint32_t)lane < n ? __ldg(bval + rowbase + ej + lane) : 0.0;
+      for (int t = 0; t < jn; ++t) {
+        const uint32_t cl = ncl, cn = n;
+        const double v = nv;
         const uint32_t dj = __shfl_sync(0xffffffffu, d_l, t);
         const uint32_t dn = t + 1 < 32 ? __shfl_sync(0xffffffffu, d_l, min(t + 1, 31)) : d_last;
-        const uint32_t n = (t + 1 == jn ? e_last : en) - ej, m = (t + 1 == jn ? d_last : dn) - dj;
-        if (n == 0) continue;
-        const bool seq = ci == kCatDense || (int64_t)n >= sem.crossover;
+        const uint32_t m = (t + 1 == jn ? d_last : dn) - dj;
+        if (t + 1 < jn) {
+          bounds(t + 1, ej, n);
+          ncl = (uint32_t)lane < n ? (uint32_t)__ldg(bcol + rowbase + ej + lane) : 0u;
+          nv = (uint32_t)lane < n ? __ldg(bval + rowbase + ej + lane) : 0.0;
+        }
+        if (cn == 0) continue;
+        const bool seq = ci == kCatDense || (int64_t)cn >= sem.crossover;
         const uint32_t colbase = (uint32_t)((rb.b0 + j0 + t) << gs) & cwmask;
-        ok &= reduce_chunk_wave(bcol + rowbase + ej, bval + rowbase + ej, n, m, seq, colbase, c_col, c_val, out_row + dj) == 1;
+        ok &= reduce_chunk_wave_core(cl, v, cn, m, seq, colbase, c_col, c_val, out_row + dj) == 1;
       }
     }
     if (!ok && lane == 0) atomicOr(err, 4ull);
