@@ -736,6 +736,10 @@ int magnus_categories(magnus_ctx* ctx, int8_t* dst, void* stream) {
 }
 
 // Heavy rows, numeric phase, binned path: batches of rows whose products fit the reorder buffer.
+#ifndef MG_BATCH_FRAC_SERIAL
+#define MG_BATCH_FRAC_SERIAL 0.3
+#endif
+static constexpr double kBatchFracSerial = MG_BATCH_FRAC_SERIAL;
 static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, double* c_val) {
   cudaStream_t s = ctx->stream;
   const int64_t nH = ctx->host_stats[mg::kStatNH];
@@ -756,7 +760,18 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     if (reserved > used) free_b += (size_t)(reserved - used);
   }
   const int64_t per_elem = 10;   // u16 local column + f64 product
-  int64_t cap = std::min<int64_t>(total, std::min<int64_t>((int64_t)(free_b * 0.2) / per_elem, int64_t(3) << 30));
+  // the reducers run on the main stream after each batch's expand (measured faster than
+  // overlapping them on side streams); MAGNUS_SERIAL=0 restores the concurrent pipeline,
+  // which needs a second buffer set
+  const char* serial_env = std::getenv("MAGNUS_SERIAL");
+  const bool serial = !(serial_env && std::strcmp(serial_env, "0") == 0);
+  // fraction of free HBM per buffer set (MAGNUS_BATCH_FRAC overrides; measured on cfg3)
+  double frac = serial ? kBatchFracSerial : 0.2;
+  if (const char* bf = std::getenv("MAGNUS_BATCH_FRAC")) {
+    const double v = std::atof(bf);
+    if (v > 0.0 && v < 0.9) frac = v;
+  }
+  int64_t cap = std::min<int64_t>(total, std::min<int64_t>((int64_t)(free_b * frac) / per_elem, int64_t(3) << 30));
   if (const char* ce = std::getenv("MAGNUS_BATCH_ELEMS")) {   // testing: force many heavy-row batches
     const long long v = std::atoll(ce);
     if (v > 0) cap = std::min<int64_t>(cap, (int64_t)v);
@@ -784,8 +799,8 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
       buf_elems = std::max(buf_elems, a);
     }
   }
-  // two buffer sets: the expand of batch b+1 overlaps the reducers of batch b
-  const int nbuf = cuts.size() > 2 ? 2 : 1;
+  // two buffer sets when the expand of batch b+1 overlaps the reducers of batch b
+  const int nbuf = (cuts.size() > 2 && !serial) ? 2 : 1;
   const int64_t max_big = std::max<int64_t>(max_ent, 1) + buf_elems / mg::kBigSplit + 1;
   void *bcol[2] = {nullptr, nullptr}, *bval[2] = {nullptr, nullptr}, *items[2] = {nullptr, nullptr},
        *cnts[2] = {nullptr, nullptr};
@@ -831,10 +846,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     MG_CUDA(cudaStreamSynchronize(s));
   }
   cudaStream_t sr = ctx->aux, sbig = ctx->aux2;
-  // the reducers run on the main stream after each batch's expand (measured faster than
-  // overlapping them on side streams); MAGNUS_SERIAL=0 restores the concurrent pipeline
-  const char* serial_env = std::getenv("MAGNUS_SERIAL");
-  if (!(serial_env && std::strcmp(serial_env, "0") == 0)) sr = sbig = s;
+  if (serial) sr = sbig = s;
   bool used[2] = {false, false};
   for (size_t b = 0; b + 1 < cuts.size(); ++b) {
     const int q = (int)(b % nbuf);
