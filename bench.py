@@ -78,6 +78,11 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's own start-up (NVML init) contends with the driver: let it finish
+            # before the timed region opens (the samples still cover the whole region)
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < float(os.environ.get("BENCH_SAMPLER_WAIT", "5")):
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
