@@ -447,21 +447,54 @@ __device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA 
       if (koff[mid] <= q_beg) lo = mid; else hi = mid;
     }
     uint32_t q = q_beg;   // positions below q are counted
-    for (int j = lo; j < nk && koff[j] < q_end; ++j) {
-      const uint32_t qa = max(q_beg, (uint32_t)koff[j]), qb = min(q_end, (uint32_t)koff[j + 1]);
-      const int32_t sl = (int32_t)kslot[j];
-      if (sl < 0 || qb - qa < 64u) continue;
-      // the piece [P0, P1) of B row j inside this range: chunks c0..c1 of the unit
-      const uint32_t P0 = kpos[j] + (qa - koff[j]), P1 = P0 + (qb - qa);
-      const uint32_t c0 = (__ldg(B.col + P0) >> shift) - cb, c1 = (__ldg(B.col + P1 - 1) >> shift) - cb;
-      if (c1 - c0 + 1 > qb - qa) continue;   // sparser than one element per chunk: count columns
-      count_range(q, qa);
-      const uint32_t* ix = bidx + (size_t)sl * nwin1 + cb;
-      for (uint32_t c = c0 + lane; c <= c1; c += 32) {
-        const uint32_t lo_c = max(P0, __ldg(ix + c)), hi_c = min(P1, __ldg(ix + c + 1));
-        sh_red_add_pred(hi_c > lo_c, a_wc + (c << 2), hi_c - lo_c);
+    // 32 segments at a time: each lane classifies one (its end columns are loaded in
+    // parallel), then the eligible ones are counted from the window index in stream order
+    for (int j0 = lo; j0 < nk && koff[j0] < q_end; j0 += 32) {
+      const int j = j0 + lane;
+      bool el = false;
+      uint32_t qa = 0, qb = 0, P0 = 0, c0 = 0, c1 = 0;
+      int32_t sl = -1;
+      if (j < nk && koff[j] < q_end) {
+        qa = max(q_beg, (uint32_t)koff[j]);
+        qb = min(q_end, (uint32_t)koff[j + 1]);
+        sl = (int32_t)kslot[j];
+        if (sl >= 0 && qb - qa >= 64u) {
+          // the piece [P0, P0 + qb - qa) of B row j inside this range: chunks c0..c1 of the unit
+          P0 = kpos[j] + (qa - koff[j]);
+          c0 = (__ldg(B.col + P0) >> shift) - cb;
+          c1 = (__ldg(B.col + P0 + (qb - qa) - 1) >> shift) - cb;
+          el = c1 - c0 + 1 <= qb - qa;   // else sparser than one element per chunk: count columns
+        }
       }
-      q = qb;
+      uint32_t m = __ballot_sync(0xffffffffu, el);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t sqa = __shfl_sync(0xffffffffu, qa, src), sqb = __shfl_sync(0xffffffffu, qb, src);
+        const uint32_t sP0 = __shfl_sync(0xffffffffu, P0, src), sP1 = sP0 + (sqb - sqa);
+        const uint32_t sc0 = __shfl_sync(0xffffffffu, c0, src), sc1 = __shfl_sync(0xffffffffu, c1, src);
+        const int32_t ssl = __shfl_sync(0xffffffffu, sl, src);
+        count_range(q, sqa);
+        const uint32_t* ix = bidx + (size_t)ssl * nwin1 + cb;
+        for (uint32_t cc = sc0; cc <= sc1; cc += 128) {
+          uint32_t lo_c[4], hi_c[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t c = cc + 32 * u + lane;
+            lo_c[u] = hi_c[u] = 0u;
+            if (c <= sc1) {
+              lo_c[u] = max(sP0, __ldg(ix + c));
+              hi_c[u] = min(sP1, __ldg(ix + c + 1));
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t c = cc + 32 * u + lane;
+            sh_red_add_pred(hi_c[u] > lo_c[u], a_wc + (c << 2), hi_c[u] - lo_c[u]);
+          }
+        }
+        q = sqb;
+      }
     }
     count_range(q, q_end);
   }
