@@ -36,6 +36,10 @@ constexpr int kS2T = MG_S2_T;              // threads per CTA
 constexpr int kS2WinLog = MG_S2_WIN;       // bitmap window: 2^20 columns (128 KB)
 constexpr int kS2Words = (1 << kS2WinLog) / 32;
 constexpr int kS2Touch = MG_S2_TOUCH;             // touched-word list (full scan of the row's words beyond it)
+#ifndef MG_S2_DENSE
+#define MG_S2_DENSE 2
+#endif
+constexpr int kS2DenseRatio = MG_S2_DENSE;  // dense window: products >= this x spanned words (0: never)
 constexpr int kS2Chunks = 2048;            // chunk counters per row
 constexpr int kS2K = MG_S2_K;                 // k's whose stream offsets live in shared memory
 #ifndef MG_S2_U
@@ -76,6 +80,10 @@ __device__ __forceinline__ uint32_t sh_atom_or_if(bool p, uint32_t addr, uint32_
                : "+r"(old) : "r"(addr), "r"((uint32_t)p), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ void sh_red_or_if(bool p, uint32_t addr, uint32_t v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q red.shared.or.b32 [%1], %2;\n}\n"
+               :: "r"((uint32_t)p), "r"(addr), "r"(v) : "memory");
+}
 __device__ __forceinline__ void sh_red_add_if(bool p, uint32_t addr, uint32_t v) {
   asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %0, 0;\n @q red.shared.add.u32 [%1], %2;\n}\n"
                :: "r"((uint32_t)p), "r"(addr), "r"(v) : "memory");
@@ -94,7 +102,9 @@ __device__ __forceinline__ void sh_st_if(bool p, uint32_t addr, uint32_t v) {
 // row's segments, koff[nk] = total; kpos: their B positions).  Marks columns, lists the
 // bitmap words that became non-zero, counts products per chunk.  KP: shared or global
 // arrays (separate instantiations keep the shared-memory case on LDS).
-template <class KP>
+// Track = false (dense windows): columns are marked without reading the old word back and
+// no touched-word list is kept; the caller scans the window's word range instead.
+template <class KP, bool Track = true>
 __device__ __forceinline__ void sym2_stream(const DevCsr& B, KP koff, KP kpos, int nk, uint32_t q_beg, uint32_t q_end,
                                             uint32_t wlo, int shift, uint32_t f0, uint32_t* bm, uint32_t* touch,
                                             uint32_t* ntouch, uint32_t* ccnt) {
@@ -162,14 +172,18 @@ __device__ __forceinline__ void sym2_stream(const DevCsr& B, KP koff, KP kpos, i
       const uint32_t c = cw[u];
       const bool valid = c != 0xffffffffu;
       const uint32_t lc = c - wlo;
-      const bool fresh = sh_atom_or_if(valid, a_bm + ((lc >> 5) << 2), 1u << (lc & 31)) == 0u;
-      const uint32_t fm = __ballot_sync(0xffffffffu, fresh);
-      if (fm) {
-        uint32_t b = 0;
-        if (lane == 0) b = sh_atom_add(a_nt, (uint32_t)__popc(fm));
-        b = __shfl_sync(0xffffffffu, b, 0);
-        const uint32_t slot = b + __popc(fm & lt);
-        sh_st_if(fresh && slot < (uint32_t)kS2Touch, a_touch + (slot << 2), lc >> 5);
+      if (Track) {
+        const bool fresh = sh_atom_or_if(valid, a_bm + ((lc >> 5) << 2), 1u << (lc & 31)) == 0u;
+        const uint32_t fm = __ballot_sync(0xffffffffu, fresh);
+        if (fm) {
+          uint32_t b = 0;
+          if (lane == 0) b = sh_atom_add(a_nt, (uint32_t)__popc(fm));
+          b = __shfl_sync(0xffffffffu, b, 0);
+          const uint32_t slot = b + __popc(fm & lt);
+          sh_st_if(fresh && slot < (uint32_t)kS2Touch, a_touch + (slot << 2), lc >> 5);
+        }
+      } else {
+        sh_red_or_if(valid, a_bm + ((lc >> 5) << 2), 1u << (lc & 31));
       }
       // products per chunk: runs of equal chunks (invalid lanes end the last run)
       const uint32_t ch = valid ? (c >> shift) - f0 : 0xffffffffu;   // row-relative chunk
@@ -243,9 +257,18 @@ k_heavy_sym2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows
       // ---- stream: warp w takes [w L, (w+1) L), L a multiple of 32
       const uint32_t L = ((T + NW - 1) / NW + 31) & ~31u;
       const uint32_t q_beg = min(T, (uint32_t)wid * L), q_end = min(T, q_beg + L);
+      // dense window (products >= kS2DenseRatio x the bitmap words the row spans in it): no
+      // touched-word list, the word range is scanned below
+      const int64_t wd_lo = (max(row_lo, wlo) - wlo) >> 5, wd_hi = (min(row_hi, whi - 1) - wlo) >> 5;
+      const bool dense = kS2DenseRatio > 0 && (int64_t)T >= (int64_t)kS2DenseRatio * (wd_hi - wd_lo + 1);
       if (q_beg < q_end) {
-        if (nk <= kS2K) sym2_stream(B, ks_off, ks_pos, nk, q_beg, q_end, (uint32_t)wlo, shift, (uint32_t)f0, bm, touch, &s_ntouch, ccnt);
-        else sym2_stream(B, koff, kpos, nk, q_beg, q_end, (uint32_t)wlo, shift, (uint32_t)f0, bm, touch, &s_ntouch, ccnt);
+        if (dense) {
+          if (nk <= kS2K) sym2_stream<uint32_t*, false>(B, ks_off, ks_pos, nk, q_beg, q_end, (uint32_t)wlo, shift, (uint32_t)f0, bm, touch, &s_ntouch, ccnt);
+          else sym2_stream<uint32_t*, false>(B, koff, kpos, nk, q_beg, q_end, (uint32_t)wlo, shift, (uint32_t)f0, bm, touch, &s_ntouch, ccnt);
+        } else {
+          if (nk <= kS2K) sym2_stream(B, ks_off, ks_pos, nk, q_beg, q_end, (uint32_t)wlo, shift, (uint32_t)f0, bm, touch, &s_ntouch, ccnt);
+          else sym2_stream(B, koff, kpos, nk, q_beg, q_end, (uint32_t)wlo, shift, (uint32_t)f0, bm, touch, &s_ntouch, ccnt);
+        }
       }
       __syncthreads();
       // ---- big chunks: keep their column bitmaps for the big-chunk reducer (k_bin_big)
@@ -268,7 +291,7 @@ k_heavy_sym2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows
       }
       // ---- distinct columns per chunk from the touched words (clear them)
       const uint32_t nt = s_ntouch;
-      if (nt <= (uint32_t)kS2Touch) {
+      if (!dense && nt <= (uint32_t)kS2Touch) {
         for (uint32_t t = threadIdx.x; t < nt; t += kS2T) {
           const uint32_t wd = touch[t];
           const uint32_t x = bm[wd];
@@ -283,7 +306,6 @@ k_heavy_sym2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows
           }
         }
       } else {
-        const int64_t wd_lo = (max(row_lo, wlo) - wlo) >> 5, wd_hi = (min(row_hi, whi - 1) - wlo) >> 5;
         for (int64_t wd = wd_lo + threadIdx.x; wd <= wd_hi; wd += kS2T) {
           const uint32_t x = bm[wd];
           if (!x) continue;
