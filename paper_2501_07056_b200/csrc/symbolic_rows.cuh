@@ -36,10 +36,10 @@ constexpr int kS2T = MG_S2_T;              // threads per CTA
 constexpr int kS2WinLog = MG_S2_WIN;       // bitmap window: 2^20 columns (128 KB)
 constexpr int kS2Words = (1 << kS2WinLog) / 32;
 constexpr int kS2Touch = MG_S2_TOUCH;             // touched-word list (full scan of the row's words beyond it)
-#ifndef MG_S2_DENSE
-#define MG_S2_DENSE 2
+#ifndef MG_S2_DENSE4
+#define MG_S2_DENSE4 2
 #endif
-constexpr int kS2DenseRatio = MG_S2_DENSE;  // dense window: products >= this x spanned words (0: never)
+constexpr int kS2Dense4 = MG_S2_DENSE4;  // dense window: 4 x products >= this x spanned words (< 0: never)
 constexpr int kS2Chunks = 2048;            // chunk counters per row
 constexpr int kS2K = MG_S2_K;                 // k's whose stream offsets live in shared memory
 #ifndef MG_S2_U
@@ -257,10 +257,10 @@ k_heavy_sym2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows
       // ---- stream: warp w takes [w L, (w+1) L), L a multiple of 32
       const uint32_t L = ((T + NW - 1) / NW + 31) & ~31u;
       const uint32_t q_beg = min(T, (uint32_t)wid * L), q_end = min(T, q_beg + L);
-      // dense window (products >= kS2DenseRatio x the bitmap words the row spans in it): no
+      // dense window (4 x products >= kS2Dense4 x the bitmap words the row spans in it): no
       // touched-word list, the word range is scanned below
       const int64_t wd_lo = (max(row_lo, wlo) - wlo) >> 5, wd_hi = (min(row_hi, whi - 1) - wlo) >> 5;
-      const bool dense = kS2DenseRatio > 0 && (int64_t)T >= (int64_t)kS2DenseRatio * (wd_hi - wd_lo + 1);
+      const bool dense = kS2Dense4 >= 0 && 4 * (int64_t)T >= (int64_t)kS2Dense4 * (wd_hi - wd_lo + 1);
       if (q_beg < q_end) {
         if (dense) {
           if (nk <= kS2K) sym2_stream<uint32_t*, false>(B, ks_off, ks_pos, nk, q_beg, q_end, (uint32_t)wlo, shift, (uint32_t)f0, bm, touch, &s_ntouch, ccnt);
