@@ -368,7 +368,7 @@ struct E2Cursor {
         return cnt;
       };
 #pragma unroll
-      for (int u = 0; u < kE2U; ++u) {
+      for (int u = 0; u < U; ++u) {
         const uint32_t q0 = q00 + 32 * u, q = q0 + lane;
         if (q0 + 31 < kend) {
           pos[u] = base + q;
@@ -387,7 +387,7 @@ struct E2Cursor {
       return;
     }
 #pragma unroll
-    for (int u = 0; u < kE2U; ++u) multi[u] = wave(q00 + 32 * u, q00 + 32 * u + lane, q_end, pos[u], seg[u]);
+    for (int u = 0; u < U; ++u) multi[u] = wave(q00 + 32 * u, q00 + 32 * u + lane, q_end, pos[u], seg[u]);
   }
 };
 
