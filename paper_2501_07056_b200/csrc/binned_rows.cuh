@@ -282,6 +282,10 @@ constexpr int kE2K = MG_E2_K;              // k's whose segments live in shared 
 #define MG_E2_U 4
 #endif
 constexpr int kE2U = MG_E2_U;              // waves in flight per warp
+#ifndef MG_E2_P1_SPLIT
+#define MG_E2_P1_SPLIT 0
+#endif
+constexpr bool kE2P1Split = MG_E2_P1_SPLIT != 0;   // pass 1 split across warps independently of ownership
 struct Exp2Smem {
   static constexpr size_t kCnt = (size_t)kE2W * kBinCur * 4;            // per warp, per chunk of the unit
   static constexpr size_t kK = (size_t)(kE2K + 32) * (4 + 4 + 8 + 4);   // koff, kpos, kav, kslot
@@ -406,6 +410,7 @@ __device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA 
   // ---- pass 1: products per chunk of this warp's range.  A B row segment that lies wholly
   // in the range and holds more elements than the unit has chunks is counted from the B
   // window index (one difference per chunk); the other positions column by column.
+  uint32_t a_p1 = a_wc;   // counters pass 1 is adding to (owner of the current range)
   auto count_range = [&](uint32_t qa, uint32_t qb) {
     if (qa >= qb) return;
     E2Cursor<KP> cur{koff, kpos, nk, 0, 0, 0};
@@ -435,68 +440,79 @@ __device__ __forceinline__ void exp2_unit(const DevCsr& B, KP koff, KP kpos, KA 
         const uint32_t hm = __ballot_sync(0xffffffffu, head);
         const uint32_t after = hm & ~le;
         const uint32_t nxt = after ? (uint32_t)(__ffs(after) - 1) : 32u;
-        sh_red_add_pred(valid && head, a_wc + (ch << 2), nxt - (uint32_t)lane);
+        sh_red_add_pred(valid && head, a_p1 + (ch << 2), nxt - (uint32_t)lane);
       }
     }
   };
-  if (q_beg < q_end) {
-    // segment of q_beg
-    int lo = 0, hi = nk;   // koff[lo] <= q_beg < koff[hi]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (koff[mid] <= q_beg) lo = mid; else hi = mid;
-    }
-    uint32_t q = q_beg;   // positions below q are counted
-    // 32 segments at a time: each lane classifies one (its end columns are loaded in
-    // parallel), then the eligible ones are counted from the window index in stream order
-    for (int j0 = lo; j0 < nk && koff[j0] < q_end; j0 += 32) {
-      const int j = j0 + lane;
-      bool el = false;
-      uint32_t qa = 0, qb = 0, P0 = 0, c0 = 0, c1 = 0;
-      int32_t sl = -1;
-      if (j < nk && koff[j] < q_end) {
-        qa = max(q_beg, (uint32_t)koff[j]);
-        qb = min(q_end, (uint32_t)koff[j + 1]);
-        sl = (int32_t)kslot[j];
-        if (sl >= 0 && qb - qa >= 64u) {
-          // the piece [P0, P0 + qb - qa) of B row j inside this range: chunks c0..c1 of the unit
-          P0 = kpos[j] + (qa - koff[j]);
-          c0 = (__ldg(B.col + P0) >> shift) - cb;
-          c1 = (__ldg(B.col + P0 + (qb - qa) - 1) >> shift) - cb;
-          el = c1 - c0 + 1 <= qb - qa;   // else sparser than one element per chunk: count columns
-        }
+  // pass 1's work split is decoupled from the owner ranges: warp w counts part
+  // (w - o) mod kE2W of every owner o's range into o's counters (red.shared: atomic), so a
+  // range of short, column-by-column pieces is spread over all warps
+  const uint32_t Ls = kE2P1Split ? (((L + kE2W - 1) / kE2W + 31) & ~31u) : L;
+  for (int oo = 0; oo < (kE2P1Split ? kE2W : 1); ++oo) {
+    const int o = kE2P1Split ? oo : wid;
+    const int jp = kE2P1Split ? ((wid - o + kE2W) % kE2W) : 0;
+    const uint32_t ob = min(T, (uint32_t)o * L), oe = min(T, ob + L);
+    const uint32_t p_beg = min(oe, ob + (uint32_t)jp * Ls), p_end = min(oe, p_beg + Ls);
+    a_p1 = (uint32_t)__cvta_generic_to_shared(cnt + (size_t)o * kBinCur);
+    if (p_beg < p_end) {
+      // segment of p_beg
+      int lo = 0, hi = nk;   // koff[lo] <= p_beg < koff[hi]
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (koff[mid] <= p_beg) lo = mid; else hi = mid;
       }
-      uint32_t m = __ballot_sync(0xffffffffu, el);
-      while (m) {
-        const int src = __ffs(m) - 1;
-        m &= m - 1;
-        const uint32_t sqa = __shfl_sync(0xffffffffu, qa, src), sqb = __shfl_sync(0xffffffffu, qb, src);
-        const uint32_t sP0 = __shfl_sync(0xffffffffu, P0, src), sP1 = sP0 + (sqb - sqa);
-        const uint32_t sc0 = __shfl_sync(0xffffffffu, c0, src), sc1 = __shfl_sync(0xffffffffu, c1, src);
-        const int32_t ssl = __shfl_sync(0xffffffffu, sl, src);
-        count_range(q, sqa);
-        const uint32_t* ix = bidx + (size_t)ssl * nwin1 + cb;
-        for (uint32_t cc = sc0; cc <= sc1; cc += 128) {
-          uint32_t lo_c[4], hi_c[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t c = cc + 32 * u + lane;
-            lo_c[u] = hi_c[u] = 0u;
-            if (c <= sc1) {
-              lo_c[u] = max(sP0, __ldg(ix + c));
-              hi_c[u] = min(sP1, __ldg(ix + c + 1));
+      uint32_t q = p_beg;   // positions below q are counted
+      // 32 segments at a time: each lane classifies one (its end columns are loaded in
+      // parallel), then the eligible ones are counted from the window index in stream order
+      for (int j0 = lo; j0 < nk && koff[j0] < p_end; j0 += 32) {
+        const int j = j0 + lane;
+        bool el = false;
+        uint32_t qa = 0, qb = 0, P0 = 0, c0 = 0, c1 = 0;
+        int32_t sl = -1;
+        if (j < nk && koff[j] < p_end) {
+          qa = max(p_beg, (uint32_t)koff[j]);
+          qb = min(p_end, (uint32_t)koff[j + 1]);
+          sl = (int32_t)kslot[j];
+          if (sl >= 0 && qb - qa >= 64u) {
+            // the piece [P0, P0 + qb - qa) of B row j inside this range: chunks c0..c1 of the unit
+            P0 = kpos[j] + (qa - koff[j]);
+            c0 = (__ldg(B.col + P0) >> shift) - cb;
+            c1 = (__ldg(B.col + P0 + (qb - qa) - 1) >> shift) - cb;
+            el = c1 - c0 + 1 <= qb - qa;   // else sparser than one element per chunk: count columns
+          }
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, el);
+        while (m) {
+          const int src = __ffs(m) - 1;
+          m &= m - 1;
+          const uint32_t sqa = __shfl_sync(0xffffffffu, qa, src), sqb = __shfl_sync(0xffffffffu, qb, src);
+          const uint32_t sP0 = __shfl_sync(0xffffffffu, P0, src), sP1 = sP0 + (sqb - sqa);
+          const uint32_t sc0 = __shfl_sync(0xffffffffu, c0, src), sc1 = __shfl_sync(0xffffffffu, c1, src);
+          const int32_t ssl = __shfl_sync(0xffffffffu, sl, src);
+          count_range(q, sqa);
+          const uint32_t* ix = bidx + (size_t)ssl * nwin1 + cb;
+          for (uint32_t cc = sc0; cc <= sc1; cc += 128) {
+            uint32_t lo_c[4], hi_c[4];
+  #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t c = cc + 32 * u + lane;
+              lo_c[u] = hi_c[u] = 0u;
+              if (c <= sc1) {
+                lo_c[u] = max(sP0, __ldg(ix + c));
+                hi_c[u] = min(sP1, __ldg(ix + c + 1));
+              }
+            }
+  #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t c = cc + 32 * u + lane;
+              sh_red_add_pred(hi_c[u] > lo_c[u], a_p1 + (c << 2), hi_c[u] - lo_c[u]);
             }
           }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t c = cc + 32 * u + lane;
-            sh_red_add_pred(hi_c[u] > lo_c[u], a_wc + (c << 2), hi_c[u] - lo_c[u]);
-          }
+          q = sqb;
         }
-        q = sqb;
       }
+      count_range(q, p_end);
     }
-    count_range(q, q_end);
   }
   __syncthreads();
   // ---- slice starts: chunk start (row-relative, from the symbolic tables) + earlier warps
