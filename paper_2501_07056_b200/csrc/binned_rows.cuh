@@ -282,6 +282,9 @@ constexpr int kE2K = MG_E2_K;              // k's whose segments live in shared 
 #define MG_E2_U 4
 #endif
 constexpr int kE2U = MG_E2_U;              // waves in flight per warp
+#ifndef MG_E2_TICKET_AHEAD
+#define MG_E2_TICKET_AHEAD 0
+#endif
 #ifndef MG_E2_P1_SPLIT
 #define MG_E2_P1_SPLIT 0
 #endif
@@ -620,12 +623,23 @@ k_bin_expand2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_
   uint32_t* scratch = reinterpret_cast<uint32_t*>(smem + Exp2Smem::kCnt + Exp2Smem::kK);
   __shared__ unsigned long long s_u;
   const uint64_t nu_front = nunit[0], nu = nu_front + nunit[5];
+#if MG_E2_TICKET_AHEAD
+  // the next ticket is taken while the current unit is expanded (its write to s_u is read
+  // after the barriers inside the unit)
+  if (threadIdx.x == 0) s_u = atomicAdd(ticket, 1ull);
+  __syncthreads();
+#endif
   while (true) {
+#if !MG_E2_TICKET_AHEAD
     if (threadIdx.x == 0) s_u = atomicAdd(ticket, 1ull);
     __syncthreads();
+#endif
     const unsigned long long u = s_u;
     __syncthreads();
     if (u >= nu) break;
+#if MG_E2_TICKET_AHEAD
+    if (threadIdx.x == 0) s_u = atomicAdd(ticket, 1ull);
+#endif
     const BinItem it = units[list_slot(u, nu_front, cap_units)];
     const int64_t i = rows[it.h];
     const int64_t a0 = A.rp(i);

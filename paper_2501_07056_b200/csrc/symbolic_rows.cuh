@@ -36,6 +36,9 @@ constexpr int kS2T = MG_S2_T;              // threads per CTA
 constexpr int kS2WinLog = MG_S2_WIN;       // bitmap window: 2^20 columns (128 KB)
 constexpr int kS2Words = (1 << kS2WinLog) / 32;
 constexpr int kS2Touch = MG_S2_TOUCH;             // touched-word list (full scan of the row's words beyond it)
+#ifndef MG_S2_TICKET_AHEAD
+#define MG_S2_TICKET_AHEAD 1
+#endif
 #ifndef MG_S2_DENSE4
 #define MG_S2_DENSE4 2
 #endif
@@ -220,12 +223,22 @@ k_heavy_sym2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows
   for (int i = threadIdx.x; i < 2 * kS2Chunks; i += kS2T) ccnt[i] = 0u;
   const int wpc = shift >= 5 ? 1 << (shift - 5) : 1;   // bitmap words per chunk
   __syncthreads();
+#if MG_S2_TICKET_AHEAD
+  // the next row is taken while the current one is marked (read after the row's barriers)
+  if (threadIdx.x == 0) s_row = (int64_t)atomicAdd(work, 1ull);
+  __syncthreads();
+#endif
   while (true) {
+#if !MG_S2_TICKET_AHEAD
     if (threadIdx.x == 0) s_row = (int64_t)atomicAdd(work, 1ull);
     __syncthreads();
+#endif
     const int64_t w = s_row;
     __syncthreads();
     if (w >= nrows) break;
+#if MG_S2_TICKET_AHEAD
+    if (threadIdx.x == 0) s_row = (int64_t)atomicAdd(work, 1ull);
+#endif
     const int64_t i = rows[w];
     const int64_t a0 = A.rp(i);
     const int nk = (int)(A.rp(i + 1) - a0);
