@@ -282,6 +282,9 @@ constexpr int kE2K = MG_E2_K;              // k's whose segments live in shared 
 #define MG_E2_U 4
 #endif
 constexpr int kE2U = MG_E2_U;              // waves in flight per warp
+#ifndef MG_RED_TICKET_AHEAD
+#define MG_RED_TICKET_AHEAD 0
+#endif
 #ifndef MG_E2_TICKET_AHEAD
 #define MG_E2_TICKET_AHEAD 0
 #endif
@@ -958,11 +961,22 @@ k_bin_reduce_tiny(const int32_t* __restrict__ rows, const int8_t* __restrict__ c
   const int shift = sem.shift_num, gs = bin_shift_of(shift);
   const int64_t nw = (int64_t)*nwin;
   const uint32_t cwmask = ~((1u << shift) - 1u);
+#if MG_RED_TICKET_AHEAD
+  // the next window's ticket is taken while the current window is reduced
+  unsigned long long wnext = 0;
+  if (lane == 0) wnext = atomicAdd(ticket, 1ull);
+#endif
   while (true) {
     unsigned long long wi = 0;
+#if MG_RED_TICKET_AHEAD
+    wi = __shfl_sync(0xffffffffu, wnext, 0);
+    if ((int64_t)wi >= nw) break;
+    if (lane == 0) wnext = atomicAdd(ticket, 1ull);
+#else
     if (lane == 0) wi = atomicAdd(ticket, 1ull);
     wi = __shfl_sync(0xffffffffu, wi, 0);
     if ((int64_t)wi >= nw) break;
+#endif
     const BinItem it = wins[wi];
     const int64_t i = rows[it.h];
     const int ci = cat[i];
@@ -1034,11 +1048,22 @@ k_bin_reduce(const int32_t* __restrict__ rows, const int8_t* __restrict__ cat, c
   S.inv = reinterpret_cast<uint16_t*>(base + w4 + w2 + (size_t)kBinE * 12);
   const int64_t nw = (int64_t)*nwin;
   const uint32_t cwmask = ~((1u << shift) - 1u);
+#if MG_RED_TICKET_AHEAD
+  // the next window's ticket is taken while the current window is reduced
+  unsigned long long wnext = 0;
+  if ((threadIdx.x & 31) == 0) wnext = atomicAdd(ticket, 1ull);
+#endif
   while (true) {
     unsigned long long wi = 0;
+#if MG_RED_TICKET_AHEAD
+    wi = __shfl_sync(0xffffffffu, wnext, 0);
+    if ((int64_t)wi >= nw) break;
+    if ((threadIdx.x & 31) == 0) wnext = atomicAdd(ticket, 1ull);
+#else
     if ((threadIdx.x & 31) == 0) wi = atomicAdd(ticket, 1ull);
     wi = __shfl_sync(0xffffffffu, wi, 0);
     if ((int64_t)wi >= nw) break;
+#endif
     const BinItem it = wins[wi];
     const int64_t i = rows[it.h];
     const int ci = cat[i];
