@@ -126,6 +126,48 @@ def config_desc(cfg):
     return names[cfg], p
 
 
+def workload_config(cfg, A, B, inter_total, world):
+    """The `config` object of the JSON line: identical in both arms (--impl ours / reference)."""
+    name, _ = config_desc(cfg)
+    return {"workload": name, "n": int(A.n_rows), "nnz_a": int(len(A.col)), "nnz_b": int(len(B.col)),
+            "inter_products": int(inter_total), "gflop": 2 * int(inter_total) / 1e9,
+            "l2": "flushed (256 MB write) before each step", "dtype": "f64 values, int32 columns",
+            "parallelism": f"rows split by flop over {world} GPU(s), B broadcast"}
+
+
+def host_system_params():
+    """The reference's detect_system_params() (planner.py:179-222) restated for the host this
+    runs on: L2 size and line of cpu0 from sysfs (64 B / 1 MiB fallbacks), memory budget a
+    quarter of physical memory."""
+    from paper_2501_07056_b200 import SystemParams
+    base = "/sys/devices/system/cpu/cpu0/cache"
+    line, l2 = None, None
+    try:
+        for e in sorted(os.listdir(base)):
+            if not e.startswith("index"):
+                continue
+            with open(f"{base}/{e}/level") as f:
+                if f.read().strip() != "2":
+                    continue
+            with open(f"{base}/{e}/size") as f:
+                sz = f.read().strip()
+            l2 = int(sz[:-1]) * (1024 if sz.endswith("K") else 1 << 20) if sz[-1] in "KM" else int(sz)
+            with open(f"{base}/{e}/coherency_line_size") as f:
+                line = int(f.read().strip())
+            break
+    except (OSError, ValueError):
+        pass
+    if not line or line & (line - 1):
+        line = 64
+    if not l2 or l2 <= 0:
+        l2 = 1 << 20
+    try:
+        mem = os.sysconf("SC_PHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    except (ValueError, OSError):
+        mem = 8 << 30
+    return SystemParams(cache_line_bytes=line, l2_bytes=l2, memory_budget_bytes=max(1, mem // 4))
+
+
 def algorithmic_bytes(A, B, inter, c_nnz_row, rp_bytes_a, rp_bytes_b):
     """Per device row class: (symbolic bytes, numeric bytes) -- reads of A, of the B rows each
     product touches (row_ptr pair + col [+ val]), and (numeric) the C row written.  The §8(d)
@@ -144,12 +186,8 @@ def algorithmic_bytes(A, B, inter, c_nnz_row, rp_bytes_a, rp_bytes_b):
         b_rp = nkm * 2 * rp_bytes_b
         sym = a_bytes - nkm * 8 + b_rp + im * 4 + rows * 8
         num = a_bytes + b_rp + im * 12 + cm * 12 + rows * 16
-        # binned heavy path: expand reads A and the B rows, writes the reorder
-        # buffer (u16 column + f64 product); the reducers read the buffer and write C
-        exp_b = a_bytes + b_rp + im * 12 + im * 10
-        red_b = im * 10 + cm * 12 + rows * 16
         out[name] = {"rows": rows, "inter": im, "nnz_c": cm, "sym_bytes": sym, "num_bytes": num,
-                     "expand_bytes": exp_b, "reduce_bytes": red_b}
+                     "a_bytes": a_bytes, "b_bytes": b_rp + im * 12, "c_bytes": cm * 12 + rows * 16}
     return out
 
 
@@ -212,7 +250,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2501_07056_b200 import MagnusPlan, _lib, detect_device_params, generate, row_intermediate_stats
-    from paper_2501_07056_b200.parallel import broadcast_csr, flop_cuts, row_block
+    from paper_2501_07056_b200.parallel import distribute, rebase
 
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
@@ -223,31 +261,39 @@ def main():
     cfg = args.config
     name, p = config_desc(cfg)
 
-    # inputs: rank 0 generates on its GPU, B broadcast over NCCL to the others
+    # inputs: rank 0 generates on its GPU; with N > 1 the exchange (B broadcast over NCCL, the
+    # flop cuts, each rank's block of A) is part of every timed step
     t_gen = time.perf_counter()
     if rank == 0:
-        A, B = generate.make_config_device(cfg, rp_dtype=torch.int64 if cfg == 5 else torch.int32)
+        A0, B0 = generate.make_config_device(cfg, rp_dtype=torch.int64 if cfg == 5 else torch.int32)
     else:
-        A = B = None
-    if world > 1:
-        same = (A is B) if rank == 0 else None
-        flag = torch.tensor([1 if same else 0], device=device)
-        dist.broadcast(flag, 0)
-        A = broadcast_csr(A, 0, device)
-        B = A if int(flag) else broadcast_csr(B, 0, device)
+        A0 = B0 = None
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     sysp = detect_device_params()
-    stats = row_intermediate_stats(A, B)
-    inter = stats.inter_size
-    cuts, total_inter = flop_cuts(inter, world)
-    lo, hi = cuts[rank], cuts[rank + 1]
-    A_loc = row_block(A, lo, hi) if world > 1 else A
+    if world > 1:
+        A_loc, B, cuts, total_inter = distribute(A0, B0, rank, world, device)
+        A = A0 if rank == 0 else A_loc
+        lo, hi = cuts[rank], cuts[rank + 1]
+    else:
+        A, B, A_loc = A0, B0, A0
+    inter_loc = row_intermediate_stats(A_loc, B).inter_size
+    if world == 1:
+        total_inter = int(inter_loc.sum())
+        lo, hi = 0, A.n_rows
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)   # > 126 MB L2
+    stream = torch.cuda.current_stream()
 
-    def step(profile=False):
-        plan = MagnusPlan(A_loc, B, sys=sysp)
+    def step(profile=False, timed=None):
+        """One job step; with N > 1 the exchange first (timed[0] brackets the local compute)."""
+        if world > 1:
+            A_blk, Bx, _, _ = distribute(A0, B0, rank, world, device)
+        else:
+            A_blk, Bx = A_loc, B
+        if timed is not None:
+            timed[0].record(stream)
+        plan = MagnusPlan(A_blk, Bx, sys=sysp)
         if profile:
             plan.ctx.profile(True)
         rp = plan.symbolic()
@@ -257,6 +303,10 @@ def main():
         if profile:
             prof["_heavy"] = plan.ctx.heavy_stats()
         plan.close()
+        if timed is not None:
+            timed[1].record(stream)
+        if world > 1:
+            rebase(C, rank, world, device)
         return C, counters, launches, prof
 
     for _ in range(args.warmup):
@@ -266,27 +316,28 @@ def main():
 
     sampler = ClockSampler(local)
     sampler.start()
-    times, launches = [], 0
-    stream = torch.cuda.current_stream()
+    times, ctimes, launches = [], [], 0
     for _ in range(args.steps):
         flush.zero_()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        C, counters, nl, _ = step()
+        C, counters, nl, _ = step(timed=(c0, c1))
         e1.record(stream)
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
+        ctimes.append(c0.elapsed_time(c1))
         launches += nl
         del C
     clocks = sampler.stop()
-    total_ms = sum(times)
+    total_ms, compute_ms = sum(times), sum(ctimes)
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+        t = torch.tensor([total_ms, compute_ms], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t)
+        total_ms, compute_ms = float(t[0]), float(t[1])
     ms_step = total_ms / args.steps
     gflops = 2.0 * total_inter / (ms_step * 1e-3) / 1e9
 
@@ -296,18 +347,23 @@ def main():
     c_nnz_row = (C.row_ptr[1:] - C.row_ptr[:-1])
     nnz_c_local = int(C.row_ptr[-1])
     rp_a = A_loc.row_ptr.element_size()
-    inter_loc = inter[lo:hi]
     ab = algorithmic_bytes(A_loc, B, inter_loc, c_nnz_row, rp_a, B.row_ptr.element_size())
     del C
     peak, peak_kind = hbm_peak()
-    kern_bytes = {"num_heavy": ab["heavy"]["num_bytes"], "sym_heavy": ab["heavy"]["sym_bytes"],
-                  "bin_expand": ab["heavy"]["expand_bytes"],
-                  # reducers: the reorder buffer slices they read (10 B per product) + the C entries they write
-                  "bin_big": hs["big_products"] * 10 + hs["big_distinct"] * 12,
-                  "bin_reduce": hs["small_products"] * 10 + hs["small_distinct"] * 12,
+    # per-kernel algorithmic bytes, SURVEY.md §8(d)'s compulsory model restricted to what each
+    # kernel must move: the heavy expand reads A and the B rows its products touch, the heavy
+    # reducers write C; the light-row kernels do all three for their rows.  The reorder buffer
+    # (10 B per product written by the expand and read back by the reducers) is NOT algorithmic:
+    # it is reported separately as intermediate traffic.
+    hv = ab["heavy"]
+    kern_bytes = {"bin_expand": hv["a_bytes"] + hv["b_bytes"],
+                  "bin_big": hs["big_distinct"] * 12, "bin_reduce": hs["small_distinct"] * 12,
+                  "num_heavy": hv["num_bytes"], "sym_heavy": hv["sym_bytes"],
                   "num_dense": ab["dense"]["num_bytes"], "sym_dense": ab["dense"]["sym_bytes"],
                   "num_block": ab["block"]["num_bytes"], "sym_block": ab["block"]["sym_bytes"],
                   "num_warp": ab["warp"]["num_bytes"], "sym_warp": ab["warp"]["sym_bytes"]}
+    inter_bytes = {"bin_expand": hv["inter"] * 10, "bin_big": hs["big_products"] * 10,
+                   "bin_reduce": hs["small_products"] * 10}
     dom = max(prof, key=lambda k: prof[k][0])
     nl_dom = max(prof[dom][1], 1)
     dom_ms = prof[dom][0] / nl_dom
@@ -315,15 +371,29 @@ def main():
     if dom_bytes is not None:
         dom_bytes = dom_bytes // nl_dom   # the class's bytes are split over its launches (row batches)
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9 if dom_bytes else None
-    # DRAM traffic per launch of that kernel from the committed ncu capture of this workload
-    traffic = None
-    try:
-        tj = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                         "r1_cfg3_traffic.json")))
-        if cfg == 3 and world == 1 and dom in tj["kernels"]:
-            traffic = tj["kernels"][dom]["dram_bytes_per_launch"]
-    except (OSError, ValueError, KeyError):
-        traffic = None
+    dom_inter = inter_bytes.get(dom, 0) // nl_dom
+    # the heavy-row numeric pipeline as one unit: A + B rows touched + C of the heavy rows
+    heavy_keys = [k for k in ("bin_plan", "bin_expand", "bin_big", "bin_reduce", "num_heavy", "dir_num", "dir_plan")
+                  if k in prof]
+    heavy_ms = sum(prof[k][0] for k in heavy_keys)
+    heavy_roof = None
+    if heavy_ms > 0:
+        hb = hv["num_bytes"]
+        heavy_roof = {"kernels": heavy_keys, "ms": round(heavy_ms, 3), "compulsory_bytes": hb,
+                      "achieved": round(hb / (heavy_ms * 1e-3) / 1e9, 1), "peak": peak,
+                      "frac": round(hb / (heavy_ms * 1e-3) / 1e9 / peak, 4), "unit": "GB/s",
+                      "intermediate_bytes": hv["inter"] * 20}
+    # DRAM traffic per launch of that kernel: a COMMITTED ncu capture of this workload (ncu cannot
+    # run inside the timed bench); null when the capture does not cover this kernel
+    traffic, traffic_file = None, None
+    for cand in ("r2_cfg3_traffic.json", "r1_cfg3_traffic.json"):
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", cand)))
+        except (OSError, ValueError):
+            continue
+        if cfg == 3 and world == 1 and dom in tj.get("kernels", {}):
+            traffic, traffic_file = tj["kernels"][dom]["dram_bytes_per_launch"], cand
+        break
     prof_share = {k: round(v[0], 3) for k, v in prof.items() if v[1]}
 
     # whole-job compulsory roofline
@@ -360,7 +430,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         A_h = A.numpy() if hasattr(A, "numpy") else A
         B_h = A_h if B is A else B.numpy()
-        cpu = cpu_baseline(A_h, B_h, sysp, args.cpu_seconds, inter.cpu().numpy())
+        cpu = cpu_baseline(A_h, B_h, host_system_params(), args.cpu_seconds, inter_loc.cpu().numpy())
 
     if rank == 0:
         line = {
@@ -376,10 +446,12 @@ def main():
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded, generated on device; BASELINE.json config shapes and value distributions)",
-            "config": {"workload": name, "n": A.n_rows, "nnz_a": int(A.col.numel()), "inter_products": total_inter,
-                       "nnz_c": nnz_c, "gflop": 2 * total_inter / 1e9, "l2": "flushed (256 MB write) before each step",
-                       "parallelism": f"rows split by flop over {world} GPU(s), B broadcast", "system_params": vars(sysp)
-                       if hasattr(sysp, "__dict__") else str(sysp)},
+            "config": workload_config(cfg, A, B, total_inter, world),
+            "nnz_c": nnz_c,
+            "system_params": {"cache_line_bytes": sysp.cache_line_bytes, "l2_bytes": sysp.l2_bytes},
+            "ms_per_step_compute_only": round(compute_ms / args.steps, 4),
+            "timing": "CUDA events on the launching stream, max over ranks; N>1 steps include the B broadcast, "
+                      "the flop cuts and the A-block exchange",
             "hbm_gbs_compulsory": round(comp / (ms_step * 1e-3) / 1e9, 1),
             "roofline_step": {"bound": "hbm", "compulsory_bytes": comp,
                               "achieved": round(comp / (ms_step * 1e-3) / 1e9, 1), "peak": peak * world,
@@ -387,9 +459,11 @@ def main():
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1) if achieved else None,
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
-                         "traffic_source": "profiles/r1_cfg3_traffic.json (ncu dram__bytes_read+write, mean per launch)"
-                         if traffic else None,
-                         "algorithmic_bytes_per_launch": dom_bytes, "ms_per_launch": round(dom_ms, 4)},
+                         "traffic_source": (f"committed ncu capture profiles/{traffic_file} (dram__bytes_read+write "
+                                            "per launch; not measured in this run)") if traffic else None,
+                         "algorithmic_bytes_per_launch": dom_bytes, "bytes_model": "SURVEY.md 8(d) compulsory share",
+                         "intermediate_bytes_per_launch": dom_inter, "ms_per_launch": round(dom_ms, 4)},
+            "roofline_heavy": heavy_roof,
             "ideal_bound": ideal,
             "kernel_ms": prof_share,
             "heavy_chunks": hs,
@@ -473,35 +547,25 @@ def run_e2e(A, B, sysp, steps, total_inter):
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference algorithm's CPU restatement (oracle/) with all host
-    threads, on bounded row samples of the same workload (rank 0 only)."""
+    """--impl reference: the reference algorithm's CPU restatement (oracle/, C + OpenMP) with all
+    host threads and the reference's own host SystemParams (detect_system_params), on bounded
+    row samples of the same workload (rank 0 only).  Inputs are generated on the host (numpy):
+    nothing of the device library is loaded in this arm."""
     if rank != 0:
         return
-    from paper_2501_07056_b200 import b200_default_params, generate
-    from paper_2501_07056_b200.generate import CONFIGS
-    name, p = config_desc(args.config)
+    from paper_2501_07056_b200 import generate
     t = time.perf_counter()
     if args.config == 5:
         print(json.dumps({"impl": "reference", "unavailable": "cfg5 host generation exceeds the bench budget"}))
         return
-    try:
-        import torch
-        if torch.cuda.is_available():
-            from paper_2501_07056_b200 import _lib
-            _lib.build()
-            A, B = generate.make_config_device(args.config)
-            A = A.numpy()
-            B = A if CONFIGS[args.config]["product"] == "AA" else B.numpy()
-        else:
-            raise RuntimeError
-    except Exception:
-        A, B = generate.make_config_cpu(args.config)
+    A, B = generate.make_config_cpu(args.config)
+    t_gen = time.perf_counter() - t
     rp = np.asarray(A.row_ptr, np.int64)
     deg = np.diff(np.asarray(B.row_ptr, np.int64))
     per = deg[np.asarray(A.col).astype(np.int64)]
     cs = np.r_[0, np.cumsum(per)]
     inter = cs[rp[1:]] - cs[rp[:-1]]
-    sysp = b200_default_params()
+    sysp = host_system_params()
     seconds = max(5.0, min(args.cpu_seconds, 30.0))
     vals = []
     for s in range(max(1, args.warmup // 3) + args.steps):
@@ -511,12 +575,13 @@ def run_reference(args, world, rank):
     v = float(np.mean([r["value"] for r in vals]))
     line = {"impl": "reference", "metric": "SpGEMM GFLOP/s (2 x mults)", "value": round(v, 5), "unit": "GFLOP/s",
             "n_gpus": world, "steps": len(vals), "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": name},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, numpy on the host)",
+            "config": workload_config(args.config, A, B, int(inter.sum()), world),
             "cpu_baseline": {"value": round(v, 5), "unit": "GFLOP/s", "cores": vals[0]["cores"], "kind": "port",
-                             "sample": vals[-1]["sample"]},
+                             "sample": vals[-1]["sample"],
+                             "system_params": {"cache_line_bytes": sysp.cache_line_bytes, "l2_bytes": sysp.l2_bytes}},
             "e2e": {"value": round(v, 5), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "wall_s": round(time.perf_counter() - t, 1)}
+            "gen_s": round(t_gen, 1), "wall_s": round(time.perf_counter() - t, 1)}
     print(json.dumps(line))
 
 

@@ -96,6 +96,13 @@ int magnus_row_stats(const magnus_csr* A, const magnus_csr* B, int64_t* inter, i
 /* Per-row categories (int8, MAGNUS_CAT_*) computed by the last magnus_setup; copies n_rows bytes to device dst. */
 int magnus_categories(magnus_ctx* ctx, int8_t* dst, void* stream);
 
+/* The library's device workspace (chunk tables, reorder buffers, per-call scratch) comes from a
+ * private stream-ordered memory pool of the current device, never from the default pool.  Freed
+ * workspace stays reserved there between calls; magnus_release_workspace() synchronises the
+ * device and returns it to the driver; magnus_workspace_reserved() = bytes the pool holds. */
+int magnus_release_workspace(void);
+int64_t magnus_workspace_reserved(void);
+
 /* Number of kernel launches issued by this context since creation (telemetry). */
 int64_t magnus_launch_count(magnus_ctx* ctx);
 

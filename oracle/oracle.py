@@ -114,6 +114,20 @@ def thresholds_tuple(th):
     return (th.sort_dense_crossover, th.sort_sweet_spot)
 
 
+def symbolic(A, B, sys, thresholds=None, force_fine_only=False, threads=0):
+    """magnus_symbolic only (reference magnus.py:420-456): C.row_ptr (int64, n_rows+1) and the counters."""
+    keep = []
+    a, b = _csr(A, keep), _csr(B, keep)
+    th = OThr(*thresholds_tuple(thresholds))
+    rp = np.empty(A.n_rows + 1, np.int64)
+    info = np.zeros(7, np.int64)
+    rc = lib().oracle_symbolic(C.byref(a), C.byref(b), C.byref(_sys(sys)), C.byref(th), int(force_fine_only),
+                               int(threads), rp.ctypes.data_as(C.c_void_p), info.ctypes.data_as(C.c_void_p))
+    if rc:
+        _raise(rc)
+    return rp
+
+
 def spgemm(A, B, sys, thresholds=None, force_fine_only=False, threads=0) -> OracleResult:
     """Full reference pipeline (stats, plans, categories, symbolic, numeric) on the CPU."""
     keep = []

@@ -62,6 +62,35 @@ static void trace_point(cudaStream_t s, const char* what) {
       return set_err(MAGNUS_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
   } while (0)
 
+// The library's device workspace comes from a private stream-ordered pool per device (never
+// the default pool: the process's other allocators are left alone).  Freed workspace stays
+// reserved in the pool between calls (no re-mapping of tens of GB per call) until
+// magnus_release_workspace() trims it.
+cudaMemPool_t workspace_pool() {
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[dev] = p;
+  }
+  return pools[dev];
+}
+
+cudaError_t mg_malloc_async(void** p, size_t bytes, cudaStream_t s) {
+  cudaMemPool_t pool = workspace_pool();
+  if (!pool) return cudaErrorMemoryAllocation;
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
 int64_t ceil_pow2(int64_t x) {
   int64_t p = 1;
   while (p < x) p <<= 1;
@@ -214,7 +243,7 @@ struct magnus_ctx {
   template <class T>
   cudaError_t alloc(T** p, size_t count) {
     void* q = nullptr;
-    cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(count, 1) * sizeof(T), stream);
+    cudaError_t e = mg_malloc_async(&q, std::max<size_t>(count, 1) * sizeof(T), stream);
     if (e == cudaSuccess) allocs.push_back(q);
     *p = static_cast<T*>(q);
     return e;
@@ -226,6 +255,21 @@ extern "C" {
 const char* magnus_last_error(void) { return g_err.c_str(); }
 const char* magnus_version(void) { return "magnus_b200 0.1 (sm_100a)"; }
 int64_t magnus_launch_count(magnus_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int magnus_release_workspace(void) {
+  cudaMemPool_t pool = workspace_pool();
+  if (!pool) return set_err(MAGNUS_CUDA, "no workspace pool");
+  MG_CUDA(cudaDeviceSynchronize());
+  MG_CUDA(cudaMemPoolTrimTo(pool, 0));
+  return MAGNUS_OK;
+}
+
+int64_t magnus_workspace_reserved(void) {
+  cudaMemPool_t pool = workspace_pool();
+  uint64_t r = 0;
+  if (pool) cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r);
+  return (int64_t)r;
+}
 
 int magnus_profile_enable(magnus_ctx* ctx, int enable) {
   if (!ctx) return set_err(MAGNUS_INPUT, "null argument");
@@ -255,7 +299,7 @@ int magnus_heavy_stats(magnus_ctx* ctx, int64_t* out4) {
   const int64_t nH = ctx->host_stats[mg::kStatNH];
   if (!ctx->ready || !ctx->have_symbolic || !ctx->binned || nH == 0) return MAGNUS_OK;
   unsigned long long* d = nullptr;
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), 32, ctx->stream));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&d), 32, ctx->stream));
   MG_CUDA(cudaMemsetAsync(d, 0, 32, ctx->stream));
   mg::k_heavy_stats<<<(unsigned)std::min<int64_t>((nH + 7) / 8, (int64_t)ctx->sm_count * 8), 256, 0, ctx->stream>>>(
       ctx->listH, nH, ctx->mn, ctx->mx, (int)ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->cd, d);
@@ -313,20 +357,7 @@ int magnus_ctx_create(magnus_ctx** out) {
   auto* c = new magnus_ctx();
   MG_CUDA(cudaGetDevice(&c->device));
   MG_CUDA(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->device));
-  {
-    // keep freed workspace (reorder buffer, chunk tables) in the stream-ordered pool between
-    // calls instead of unmapping it at every synchronisation: up to a quarter of HBM
-    size_t fr = 0, tot = 0;
-    MG_CUDA(cudaMemGetInfo(&fr, &tot));
-    cudaMemPool_t pool;
-    MG_CUDA(cudaDeviceGetDefaultMemPool(&pool, c->device));
-    uint64_t thr = 0;
-    MG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    if (thr < tot / 4) {
-      thr = tot / 4;
-      MG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    }
-  }
+  if (!workspace_pool()) return set_err(MAGNUS_CUDA, "cudaMemPoolCreate failed");
   MG_CUDA(cudaFuncSetAttribute(mg::k_rows_block<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mg::kBSmem));
   MG_CUDA(cudaFuncSetAttribute(mg::k_rows_block<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mg::kBSmem));
   MG_CUDA(cudaFuncSetAttribute(mg::k_rows_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -477,8 +508,8 @@ static int launch_direct(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   const int64_t cap = std::max<int64_t>(ctx->total_ent, 1);
   void* items = nullptr;
   unsigned long long* cnt = nullptr;
-  MG_CUDA(cudaMallocAsync(&items, (size_t)cap * sizeof(mg::DirItem), s));
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cnt), 64, s));
+  MG_CUDA(mg_malloc_async(&items, (size_t)cap * sizeof(mg::DirItem), s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&cnt), 64, s));
   MG_CUDA(cudaMemsetAsync(cnt, 0, 64, s));
   ctx->begin(MAGNUS_K_DIR_PLAN);
   mg::k_dir_plan<<<(unsigned)std::min<int64_t>((nH + 7) / 8, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
@@ -496,6 +527,42 @@ static int launch_direct(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   MG_CUDA(cudaGetLastError());
   MG_CUDA(cudaFreeAsync(items, s));
   MG_CUDA(cudaFreeAsync(cnt, s));
+  return MAGNUS_OK;
+}
+
+// Device check of both operands (k_validate); err[1] collects the flags.  Out-of-range columns
+// of B are the reference's ContractViolation (magnus.py:208-209, 245-246); malformed row_ptr,
+// A columns outside B's rows and non-canonical rows are InputError (validate_csr).
+static int validate_inputs(magnus_ctx* ctx, const magnus_csr& A, const magnus_csr& B, cudaStream_t s) {
+  const bool same = A.row_ptr == B.row_ptr && A.col == B.col && A.n_rows == B.n_rows;
+  auto launch = [&](const magnus_csr& m, unsigned long long* f) {
+    const int64_t warps = std::max<int64_t>(1, std::min<int64_t>(m.n_rows, (int64_t)ctx->sm_count * 64));
+    mg::k_validate<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(dev_csr(m), f);
+    ++ctx->launches;
+  };
+  unsigned long long* fb = nullptr;
+  MG_CUDA(ctx->alloc(&fb, 2));
+  MG_CUDA(cudaMemsetAsync(fb, 0, 16, s));
+  launch(A, fb);
+  if (!same) launch(B, fb + 1);
+  MG_CUDA(cudaGetLastError());
+  unsigned long long h[2] = {0, 0};
+  MG_CUDA(cudaMemcpyAsync(h, fb, 16, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  if (same) h[1] = h[0];
+  auto bad = [](const char* which, unsigned long long f) -> std::string {
+    std::string m = std::string(which) + ": ";
+    if (f & 1) return m + "row_ptr is not a valid CSR row pointer (row_ptr[0] != 0, decreasing, or row_ptr[-1] != nnz)";
+    if (f & 2) return m + "column index out of range";
+    return m + "columns not strictly increasing within a row (non-canonical input: sort each row and sum "
+               "duplicates first; the device path requires canonical rows)";
+  };
+  if (h[0] & 1) return set_err(MAGNUS_INPUT, bad("A", h[0]));
+  if (h[1] & 1) return set_err(MAGNUS_INPUT, bad("B", h[1]));
+  if (h[0] & 2) return set_err(MAGNUS_INPUT, bad("A", 2) + " (A column >= B.n_rows)");
+  if (h[1] & 2) return set_err(MAGNUS_CONTRACT, "column index outside the planned fine-level span (B column >= n_cols)");
+  if (h[0] & 4) return set_err(MAGNUS_INPUT, bad("A", 4));
+  if (h[1] & 4) return set_err(MAGNUS_INPUT, bad("B", 4));
   return MAGNUS_OK;
 }
 
@@ -554,6 +621,11 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   MG_CUDA(cudaMemsetAsync(ctx->stats, 0, mg::kStatLen * 8, s));
   MG_CUDA(cudaMemsetAsync(ctx->err, 0, 16, s));
   {
+    // input contract before anything indexes through A or B (validate_csr matrix.py:119-150)
+    int rc0 = validate_inputs(ctx, *A, *B, s);
+    if (rc0) return rc0;
+  }
+  {
     const int64_t nskip = (B->nnz + 31) / 32;
     MG_CUDA(ctx->alloc(&ctx->skip, nskip + 1));
     if (nskip > 0) {
@@ -587,14 +659,29 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   ctx->coarse_batches = 0;
   const int64_t ncoarse = ctx->host_stats[mg::kStatNCoarse];
   if (ncoarse > 0) {
+    // (row, inter) of every coarse row: one device gather + two copies, then the reference's
+    // ascending row order on the host
     std::vector<int32_t> rows(ncoarse);
-    MG_CUDA(cudaMemcpyAsync(rows.data(), ctx->listCoarse, ncoarse * 4, cudaMemcpyDeviceToHost, s));
-    MG_CUDA(cudaStreamSynchronize(s));
-    std::sort(rows.begin(), rows.end());
     std::vector<int64_t> inter(ncoarse);
-    for (int64_t j = 0; j < ncoarse; ++j)
-      MG_CUDA(cudaMemcpyAsync(&inter[j], ctx->inter + rows[j], 8, cudaMemcpyDeviceToHost, s));
-    MG_CUDA(cudaStreamSynchronize(s));
+    {
+      int64_t* g = nullptr;
+      MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&g), (size_t)ncoarse * 8, s));
+      mg::k_gather_i64<<<(unsigned)std::min<int64_t>((ncoarse + 255) / 256, (int64_t)ctx->sm_count * 8), 256, 0, s>>>(
+          ctx->inter, ctx->listCoarse, ncoarse, g);
+      ++ctx->launches;
+      MG_CUDA(cudaGetLastError());
+      std::vector<int64_t> gi(ncoarse);
+      MG_CUDA(cudaMemcpyAsync(rows.data(), ctx->listCoarse, ncoarse * 4, cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaMemcpyAsync(gi.data(), g, ncoarse * 8, cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaFreeAsync(g, s));
+      MG_CUDA(cudaStreamSynchronize(s));
+      std::vector<int64_t> order(ncoarse);
+      for (int64_t j = 0; j < ncoarse; ++j) order[j] = j;
+      std::sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return rows[x] < rows[y]; });
+      std::vector<int32_t> r2(ncoarse);
+      for (int64_t j = 0; j < ncoarse; ++j) { r2[j] = rows[order[j]]; inter[j] = gi[order[j]]; }
+      rows.swap(r2);
+    }
     const int64_t ncc = ctx->plan_sym.n_chunks_coarse, budget = sys->memory_budget_bytes;
     const int64_t bpe = (B->n_cols <= (int64_t(1) << 32) ? 4 : 8) + sys->val_bytes;   // magnus.py:414-417
     int64_t cur_n = 0, cur_bytes = 0, cur_meta = 0, nb = 0;
@@ -635,7 +722,7 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     // order): batches then complete contiguous row ranges (the host readback overlaps them)
     // and their contents do not depend on atomic order
     int64_t* pos = nullptr;
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&pos), (size_t)(n + 1) * 8, s));
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&pos), (size_t)(n + 1) * 8, s));
     const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sm_count * 16);
     mg::k_heavy_flags<<<g, 256, 0, s>>>(ctx->inter, n, ctx->counts);
     const int64_t tiles = (n + mg::kScanTile - 1) / mg::kScanTile;
@@ -752,8 +839,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   MG_CUDA(cudaMemGetInfo(&free_b, &tot_b));
   {
     // memory the pool holds but does not use is available too
-    cudaMemPool_t pool;
-    MG_CUDA(cudaDeviceGetDefaultMemPool(&pool, ctx->device));
+    cudaMemPool_t pool = workspace_pool();
     uint64_t reserved = 0, used = 0;
     MG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
     MG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
@@ -806,12 +892,12 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
        *cnts[2] = {nullptr, nullptr};
   for (int q = 0; q < nbuf; ++q) {
     // (+64 bytes: bulk copies read 16-byte aligned supersets of a slice)
-    MG_CUDA(cudaMallocAsync(&bcol[q], (size_t)std::max<int64_t>(buf_elems, 1) * 2 + 64, s));
-    MG_CUDA(cudaMallocAsync(&bval[q], (size_t)std::max<int64_t>(buf_elems, 1) * 8 + 64, s));
+    MG_CUDA(mg_malloc_async(&bcol[q], (size_t)std::max<int64_t>(buf_elems, 1) * 2 + 64, s));
+    MG_CUDA(mg_malloc_async(&bval[q], (size_t)std::max<int64_t>(buf_elems, 1) * 8 + 64, s));
     // windows and units: <= one per chunk entry; big-chunk parts: <= entries + elements / kBigSplit
-    MG_CUDA(cudaMallocAsync(&items[q], (size_t)std::max<int64_t>(max_ent, 1) * 3 * sizeof(mg::BinItem) +
+    MG_CUDA(mg_malloc_async(&items[q], (size_t)std::max<int64_t>(max_ent, 1) * 3 * sizeof(mg::BinItem) +
                                            (size_t)max_big * 2 * sizeof(mg::BigItem), s));
-    MG_CUDA(cudaMallocAsync(&cnts[q], 128, s));
+    MG_CUDA(mg_malloc_async(&cnts[q], 128, s));
   }
   const size_t big_smem = mg::bin_big_smem(ctx->sem.shift_num, mg::kBigD);
   const size_t big_smem_w = mg::bin_big_smem(ctx->sem.shift_num, mg::kBigDWide);
@@ -828,7 +914,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   occ_e2 = std::max(occ_e2, 1);
   uint32_t* e2scr = nullptr;   // per-CTA segment tables of units with more than kE2K k's
   const int64_t e2_stride = ((ctx->host_stats[mg::kStatMaxNk] + 8 + 3) / 4) * 4;
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&e2scr), (size_t)ctx->sm_count * occ_e2 * 5 * e2_stride * 4, s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&e2scr), (size_t)ctx->sm_count * occ_e2 * 5 * e2_stride * 4, s));
   std::vector<int64_t> hb(cuts.size());
   {
     int64_t a = 0;
@@ -1167,7 +1253,7 @@ static int gd_launch(const magnus_csr* A, const magnus_csr* B, int numeric, cons
   uint32_t* bm = static_cast<uint32_t*>(scratch);
   double* acc = reinterpret_cast<double*>(bm + (size_t)ctas * nwords + ((size_t)ctas * nwords & 1));
   unsigned long long* flags = nullptr;
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&flags), 16, s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&flags), 16, s));
   MG_CUDA(cudaMemsetAsync(flags, 0, 16, s));
   MG_CUDA(cudaMemsetAsync(bm, 0, (size_t)ctas * nwords * 4, s));
   const mg::DevCsr dA = dev_csr(*A), dB = dev_csr(*B);
@@ -1184,7 +1270,7 @@ static int gd_launch(const magnus_csr* A, const magnus_csr* B, int numeric, cons
     // from the same thread)
     const int64_t tiles = (n + mg::kScanTile - 1) / mg::kScanTile;
     int64_t* tile_sums = nullptr;
-    MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tile_sums), (size_t)(tiles + 1) * 8, s));
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&tile_sums), (size_t)(tiles + 1) * 8, s));
     mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(rp_out, n, tile_sums);
     mg::k_scan_tiles<<<1, 1024, 0, s>>>(tile_sums, tiles);
     mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(rp_out, n, tile_sums, rp_out);
@@ -1243,7 +1329,7 @@ int magnus_esc_compress(const uint64_t* keys, const int64_t* perm, const double*
   mg::k_esc_heads<<<g, 256, 0, s>>>(keys, n, run_scratch);
   const int64_t tiles = (n + mg::kScanTile - 1) / mg::kScanTile;
   int64_t* tile_sums = nullptr;
-  MG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&tile_sums), (size_t)(tiles + 1) * 8, s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&tile_sums), (size_t)(tiles + 1) * 8, s));
   mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(run_scratch, n, tile_sums);
   mg::k_scan_tiles<<<1, 1024, 0, s>>>(tile_sums, tiles);
   mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(run_scratch, n, tile_sums, run_scratch);

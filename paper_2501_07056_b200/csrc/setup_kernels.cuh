@@ -40,6 +40,37 @@ __global__ void k_row_stats(DevCsr A, DevCsr B, int64_t* __restrict__ inter, int
   }
 }
 
+// Input contract of the device path, checked before any kernel indexes through the
+// inputs (validate_csr matrix.py:119-150; magnus.py:208-209, 245-246 raise
+// ContractViolation for columns outside the planned span).  One warp per row, lanes over
+// adjacent pairs (coalesced).  flags: 1 = row_ptr not monotone / row_ptr[0] != 0 /
+// row_ptr[n] != nnz, 2 = column >= n_cols, 4 = columns not strictly increasing in a row
+// (unsorted or duplicate columns: the device kernels require canonical rows).
+__global__ void k_validate(DevCsr M, unsigned long long* __restrict__ flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t ncols = (uint64_t)M.n_cols;
+  unsigned f = 0;
+  if (warp == 0 && lane == 0) {
+    if (M.rp(0) != 0 || M.rp(M.n_rows) != M.nnz) f |= 1u;
+  }
+  for (int64_t i = warp; i < M.n_rows; i += nwarps) {
+    const int64_t a0 = M.rp(i), a1 = M.rp(i + 1);
+    if (a1 < a0 || a0 < 0 || a1 > M.nnz) {
+      f |= 1u;
+      continue;
+    }
+    for (int64_t t = a0 + lane; t < a1; t += 32) {
+      const uint32_t c = __ldg(M.col + t);
+      if ((uint64_t)c >= ncols) f |= 2u;
+      if (t + 1 < a1 && __ldg(M.col + t + 1) <= c) f |= 4u;
+    }
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (lane == 0 && f) atomicOr(flags, (unsigned long long)f);
+}
+
 // Device row classes (execution strategy only; results never depend on them).
 constexpr int kClsNone = -1, kClsWarp = 0, kClsBlock = 1, kClsHeavy = 2;
 constexpr int64_t kWarpMax = 256;    // <= 256 intermediate elements: one warp, smem bitonic
@@ -244,6 +275,13 @@ __global__ void k_scan_apply(const int64_t* __restrict__ in, int64_t n, const in
     run += v[j];
     if (idx == n - 1) out[n] = run;
   }
+}
+
+// out[j] = v[idx[j]] (the coarse rows' intermediate sizes for build_coarse_batches)
+__global__ void k_gather_i64(const int64_t* __restrict__ v, const int32_t* __restrict__ idx, int64_t n,
+                             int64_t* __restrict__ out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    out[j] = v[idx[j]];
 }
 
 }  // namespace mg

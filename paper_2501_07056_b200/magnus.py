@@ -231,3 +231,82 @@ def row_intermediate_stats(A: CsrMatrix, B: CsrMatrix) -> RowStats:
     _lib.check(_lib.lib().magnus_row_stats(C.byref(a), C.byref(b), C.c_void_p(inter.data_ptr()), C.c_void_p(mn.data_ptr()),
                                            C.c_void_p(mx.data_ptr()), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     return RowStats(inter, mn, mx)
+
+
+def categorize_rows(stats: RowStats, plan, sys: SystemParams, thresholds: AccumThresholds) -> RowCategories:
+    """Reference magnus.py:68-94 (first matching rule wins): Sort if inter < crossover, Dense if
+    the row's column window fits l2 at the numeric cost (val_bytes + 1 per column), else Fine --
+    or Coarse for every such row when the plan uses the coarse level.  Works on numpy arrays and
+    on torch tensors (device-resident stats from `row_intermediate_stats` stay on the device);
+    the device pipeline applies the same rule in k_categorize."""
+    inter, rng = stats.inter_size, stats.range_len
+    is_sort = inter < thresholds.sort_dense_crossover
+    is_dense = ~is_sort & (rng * (sys.val_bytes + 1) <= sys.l2_bytes)
+    rest = ~is_sort & ~is_dense
+    none = is_sort & ~is_sort
+    is_fine, is_coarse = (none, rest) if plan.use_coarse else (rest, none)
+    if isinstance(inter, np.ndarray):
+        idx = np.flatnonzero
+    else:
+        def idx(m):
+            return _torch().nonzero(m).flatten()
+    return RowCategories(idx(is_sort), idx(is_dense), idx(is_fine), idx(is_coarse))
+
+
+# The two phases as separate calls with the reference's signatures (magnus.py:420, 459).  The
+# device keeps per-row chunk tables between them; a numeric call reuses the plan of the symbolic
+# call that produced its row_ptr, and otherwise runs the symbolic pass itself first.
+_LAST_PLAN = {}
+
+
+def _force_fine_from(plan, sys, n_cols) -> bool:
+    full = compute_chunk_plan(sys, max(n_cols, 1), SYMBOLIC, allow_coarse=True)
+    return bool(full.use_coarse and not plan.use_coarse)
+
+
+def magnus_symbolic(A, B, plan, cats, stats, sys, thresholds, threads: int = 1):
+    """Reference magnus_symbolic (magnus.py:420-456): the exact C.row_ptr (int64; numpy for host
+    inputs, a device tensor for device inputs).  `plan` is the symbolic ChunkPlan (its use_coarse
+    selects force_fine_only); categories and stats are recomputed on the device by the same rules
+    (`cats`/`stats` are accepted for API compatibility); `threads` is host-side only."""
+    _check_dims(A, B)
+    thresholds = thresholds if thresholds is not None else AccumThresholds()
+    mp = MagnusPlan(A, B, sys, thresholds, force_fine_only=_force_fine_from(plan, sys, B.n_cols))
+    rp = mp.symbolic()
+    out = rp.cpu().numpy() if mp.host_io else rp
+    _LAST_PLAN.clear()
+    _LAST_PLAN[id(out)] = (mp, rp, out)
+    return out
+
+
+def magnus_numeric(A, B, row_ptr, plan, cats, stats, sys, thresholds, threads: int = 1) -> SpgemmResult:
+    """Reference magnus_numeric (magnus.py:459-542): fills C for a row_ptr from magnus_symbolic;
+    ContractViolation if row_ptr is not the symbolic pass's result for (A, B)."""
+    _check_dims(A, B)
+    n = A.n_rows
+    shape = tuple(row_ptr.shape)
+    if shape != (n + 1,) or int(row_ptr[0]) != 0:
+        raise ContractViolation("row_ptr does not come from a symbolic pass of (A, B)")
+    thresholds = thresholds if thresholds is not None else AccumThresholds()
+    hit = _LAST_PLAN.pop(id(row_ptr), None)
+    t0 = time.perf_counter()
+    if hit is not None and hit[2] is row_ptr:
+        mp, rp = hit[0], hit[1]
+    else:
+        # plan is the numeric ChunkPlan here; coarse use is decided the same way
+        mp = MagnusPlan(A, B, sys, thresholds, force_fine_only=_force_fine_from(plan, sys, B.n_cols))
+        rp = mp.symbolic()
+        mine = rp.cpu().numpy() if mp.host_io else rp
+        same = np.array_equal(mine, np.asarray(row_ptr)) if mp.host_io else bool((mine == row_ptr.to(mine.device)).all())
+        if not same:
+            mp.close()
+            raise ContractViolation("row_ptr does not come from a symbolic pass of (A, B)")
+    Cd, counters = mp.numeric(rp)
+    mp.stream.synchronize()
+    t1 = time.perf_counter()
+    Cm = Cd
+    if mp.host_io:
+        Cm = CsrMatrix(Cd.n_rows, Cd.n_cols, np.asarray(row_ptr), Cd.col.cpu().numpy().view(np.uint32),
+                       Cd.val.cpu().numpy(), canonical=True)
+    mp.close()
+    return SpgemmResult(Cm, {"numeric": t1 - t0}, counters)

@@ -48,12 +48,16 @@ def _inter_np(A, B):
     return torch.from_numpy(cs[rp[1:]] - cs[rp[:-1]])
 
 
-def _worker(rank, world, port, outdir):
+def _worker(rank, world, port, outdir, ab=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    A = _to_torch(generate.rmat(11, 8, seed=17)) if rank == 0 else None
-    blk = spgemm_magnus_distributed(A, A, sys=SYS, local_fn=_local_oracle, inter_fn=_inter_np)
+    if ab:
+        A = _to_torch(generate.uniform_rows(3000, 4096, 6, seed=3)) if rank == 0 else None
+        B = _to_torch(generate.rmat(12, 8, seed=5)) if rank == 0 else None
+    else:
+        A = B = _to_torch(generate.rmat(11, 8, seed=17)) if rank == 0 else None
+    blk = spgemm_magnus_distributed(A, B, sys=SYS, local_fn=_local_oracle, inter_fn=_inter_np)
     np.savez(os.path.join(outdir, f"r{rank}.npz"), lo=blk.row_lo, hi=blk.row_hi, rp=blk.C.row_ptr.numpy(),
              col=blk.C.col.numpy(), val=blk.C.val.numpy(), total=blk.nnz_total)
     dist.destroy_process_group()
@@ -66,13 +70,18 @@ def test_flop_cuts_balance():
     assert all(a <= b for a, b in zip(cuts, cuts[1:]))
 
 
-def test_two_rank_gloo_equals_single(tmp_path):
+@pytest.mark.parametrize("ab", [False, True])
+def test_two_rank_gloo_equals_single(tmp_path, ab):
+    """C = A·A (A block sliced from the replicated B) and C = A·B (A blocks sent point-to-point)."""
     from oracle import oracle
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), ab), nprocs=world, join=True)
     parts = [np.load(tmp_path / f"r{r}.npz") for r in range(world)]
-    A = generate.rmat(11, 8, seed=17)
-    ref = oracle.spgemm(A, A, SYS)
+    if ab:
+        A, B = generate.uniform_rows(3000, 4096, 6, seed=3), generate.rmat(12, 8, seed=5)
+    else:
+        A = B = generate.rmat(11, 8, seed=17)
+    ref = oracle.spgemm(A, B, SYS)
     assert parts[0]["lo"] == 0 and parts[-1]["hi"] == A.n_rows and parts[0]["hi"] == parts[1]["lo"]
     rp = np.concatenate([parts[0]["rp"][:-1], parts[1]["rp"]])
     np.testing.assert_array_equal(rp, ref.row_ptr)

@@ -1,16 +1,25 @@
 """BASELINE.json configurations at full size on the B200.
 
-* cfg1, cfg2: the whole C against the CPU oracle, bit-exact.
-* cfg3, cfg4: C computed in full on the device; checked with size-independent
-  properties (canonical rows, row_ptr consistency with an independent per-row
-  distinct count, scaling A by 2 scales C exactly, run-to-run determinism),
-  and a stratified row sample (heaviest rows + random rows per inter decile)
-  against the oracle, bit-exact.  Rows are independent, so A[rows]·B equals
-  those rows of A·B.
+* cfg1, cfg2, cfg4: the whole C against the CPU oracle, bit-exact.
+* cfg3: C computed in full on the device; the WHOLE row_ptr against the
+  oracle's symbolic pass (magnus_symbolic restated, every row); the 64
+  heaviest rows (no cap: up to 9.7M products per row, the rows that exercise
+  the split big-chunk path) plus a random sample per inter decile against the
+  oracle's numeric pass, bit-exact; structural checks (canonical rows),
+  linearity ((2A).A == 2(A.A) exactly) and a checksum of the whole C.
+  Rows are independent, so A[rows]·B equals those rows of A·B.
 * cfg5 (C ~ 1.3e12 nnz does not fit any number of B200s):
-  generated in full on the device; a row sample is multiplied and checked
-  against the oracle.
+  generated in full on the device; the 32 heaviest rows (up to 3.2e8 products
+  each) and a per-decile sample are multiplied and checked bit-exact.
+* default parameters vs the reference's: the call a user makes
+  (`sys=None`, the B200 parameters) against the oracle run with the
+  reference's own host defaults (`detect_system_params`: 64 B lines, 2 MiB
+  L2) -- the north-star tolerance (pattern bit-exact, values within 1e-12
+  relative allowing for summation order, i.e. |Δ| <= 1e-12 · Σ_k |a_ik b_kj|).
 """
+
+import json
+import os
 
 import numpy as np
 import pytest
@@ -23,6 +32,18 @@ from paper_2501_07056_b200 import CsrMatrix, SystemParams, generate, spgemm_magn
 pytestmark = pytest.mark.gpu
 
 B200 = SystemParams(cache_line_bytes=128, l2_bytes=232448, memory_budget_bytes=1 << 31)
+# the reference's detect_system_params() on the hosts it was measured on
+HOST_DEFAULT = SystemParams(cache_line_bytes=64, l2_bytes=2 << 20, memory_budget_bytes=1 << 34)
+ORACLE_THREADS = min(os.cpu_count() or 1, 32)
+OUT_DIR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+
+
+def _record(name, payload):
+    """Evidence for the round report: gpurun_out/<name>.json when that directory exists."""
+    if os.path.isdir(OUT_DIR):
+        with open(os.path.join(OUT_DIR, name + ".json"), "w") as f:
+            json.dump(payload, f, indent=1)
+    print(name, payload)
 
 
 def _rows_of(A, rows):
@@ -43,10 +64,11 @@ def _inter(A, B):
     return cs[rp[1:]] - cs[rp[:-1]]
 
 
-def _sample_rows(inter, n_top=48, per_decile=24, seed=0, max_inter=None):
+def _sample_rows(inter, n_top=64, per_decile=24, seed=0):
+    """The n_top heaviest rows (no cap) plus per_decile random rows of every inter decile."""
     rng = np.random.default_rng(seed)
-    ok = np.flatnonzero(inter > 0) if max_inter is None else np.flatnonzero((inter > 0) & (inter <= max_inter))
-    order = ok[np.argsort(inter[ok])]
+    ok = np.flatnonzero(inter > 0)
+    order = ok[np.argsort(inter[ok], kind="stable")]
     rows = set(order[-n_top:].tolist()) if n_top > 0 else set()
     for d in range(10):
         part = order[d * order.size // 10:(d + 1) * order.size // 10]
@@ -55,30 +77,65 @@ def _sample_rows(inter, n_top=48, per_decile=24, seed=0, max_inter=None):
     return np.array(sorted(rows), dtype=np.int64)
 
 
-def _check_rows_against_oracle(A_h, B_h, Cg_rp, Cg_col, Cg_val, rows, sysp):
-    sub = _rows_of(A_h, rows)
-    ref = oracle.spgemm(sub, B_h, sysp)
-    rp = Cg_rp
-    got_cols, got_vals, got_rp = [], [], [0]
+def _dev(m):
+    return CsrMatrix(m.n_rows, m.n_cols, torch.from_numpy(np.asarray(m.row_ptr)).cuda(),
+                     torch.from_numpy(np.asarray(m.col)).cuda(), torch.from_numpy(np.asarray(m.val)).cuda())
+
+
+def _gather_rows(C, rows):
+    """(row_ptr, col, val) of C's rows `rows` as host numpy (C stays on the device)."""
+    rp = C.row_ptr.cpu().numpy()
+    cols, vals, out_rp = [], [], [0]
     for r in rows:
         a, b = int(rp[r]), int(rp[r + 1])
-        got_cols.append(Cg_col[a:b])
-        got_vals.append(Cg_val[a:b])
-        got_rp.append(got_rp[-1] + b - a)
-    np.testing.assert_array_equal(np.array(got_rp), ref.row_ptr)
-    np.testing.assert_array_equal(np.concatenate(got_cols).view(np.uint32), ref.col)
-    np.testing.assert_array_equal(np.concatenate(got_vals).view(np.uint64), ref.val.view(np.uint64))
+        cols.append(C.col[a:b].cpu().numpy())
+        vals.append(C.val[a:b].cpu().numpy())
+        out_rp.append(out_rp[-1] + b - a)
+    cat = (lambda xs, dt: np.concatenate(xs) if xs else np.empty(0, dt))
+    return np.array(out_rp, np.int64), cat(cols, np.int32), cat(vals, np.float64)
+
+
+def _assert_rows_bitexact(C, rows, ref):
+    rp, col, val = _gather_rows(C, rows)
+    np.testing.assert_array_equal(rp, ref.row_ptr)
+    np.testing.assert_array_equal(col.view(np.uint32), ref.col)
+    np.testing.assert_array_equal(val.view(np.uint64), ref.val.view(np.uint64))
+
+
+def _abs(m):
+    return CsrMatrix(m.n_rows, m.n_cols, m.row_ptr, m.col, np.abs(np.asarray(m.val)), m.canonical)
+
+
+def _tolerance(got, ref, absref):
+    """max strict relative error over entries with ref != 0, and max |Δ| / Σ|a_ik b_kj|."""
+    d = np.abs(got - ref)
+    nz = ref != 0
+    strict = float((d[nz] / np.abs(ref[nz])).max()) if nz.any() else 0.0
+    canc = float((d / np.where(absref > 0, absref, 1.0)).max()) if d.size else 0.0
+    return strict, canc, int((d != 0).sum())
 
 
 @pytest.mark.parametrize("cfg", [1, 2])
 def test_small_configs_full_oracle(cfg):
     A, B = generate.make_config_cpu(cfg)
-    ref = oracle.spgemm(A, B, B200)
+    ref = oracle.spgemm(A, B, B200, threads=ORACLE_THREADS)
     res = spgemm_magnus(A, B, sys=B200)
     np.testing.assert_array_equal(res.C.row_ptr, ref.row_ptr)
     np.testing.assert_array_equal(res.C.col, ref.col)
     np.testing.assert_array_equal(res.C.val.view(np.uint64), ref.val.view(np.uint64))
     assert res.counters == ref.counters
+
+
+def test_cfg4_full_oracle():
+    """cfg4 (2^23 x 2^23 uniform A·B, 5.4e8 products, 100% Sort rows): every entry, bit-exact."""
+    A, B = generate.make_config_device(4)
+    res = spgemm_magnus(A, B, sys=B200)
+    A_h, B_h = A.numpy(), B.numpy()
+    ref = oracle.spgemm(A_h, B_h, B200, threads=ORACLE_THREADS)
+    assert res.counters == ref.counters
+    np.testing.assert_array_equal(res.C.row_ptr.cpu().numpy(), ref.row_ptr)
+    np.testing.assert_array_equal(res.C.col.cpu().numpy().view(np.uint32), ref.col)
+    np.testing.assert_array_equal(res.C.val.cpu().numpy().view(np.uint64), ref.val.view(np.uint64))
 
 
 def test_device_generator_matches_numpy():
@@ -121,32 +178,26 @@ def _checksum(Cd, scale=1.0):
     return s1, s2
 
 
-@pytest.mark.parametrize("cfg", [3, 4])
-def test_large_configs(cfg):
-    A, B = generate.make_config_device(cfg, rp_dtype=torch.int32)
+def test_cfg3_full():
+    A, B = generate.make_config_device(3, rp_dtype=torch.int32)
     res = spgemm_magnus(A, B, sys=B200)
     C = res.C
     _structural(C, A.n_rows, B.n_cols)
     nnz = int(C.row_ptr[-1])
     assert res.counters["nnz_c"] == nnz
-    # stratified row sample against the oracle (bit-exact)
     A_h = A.numpy()
-    B_h = A_h if B is A else B.numpy()
-    inter = _inter(A_h, B_h)
+    inter = _inter(A_h, A_h)
     assert res.counters["inter_prod_size"] == int(inter.sum())
-    rows = _sample_rows(inter, max_inter=3_000_000)
-    rp = C.row_ptr.cpu().numpy()
-    # only the sampled rows are copied back
-    sel_col, sel_val = [], []
-    for r in rows:
-        a, b = int(rp[r]), int(rp[r + 1])
-        sel_col.append(C.col[a:b].cpu().numpy())
-        sel_val.append(C.val[a:b].cpu().numpy())
-    fake_rp = np.zeros(A.n_rows + 1, np.int64)
-    lens = np.zeros(A.n_rows, np.int64)
-    lens[rows] = rp[rows + 1] - rp[rows]
-    np.cumsum(lens, out=fake_rp[1:])
-    _check_rows_against_oracle(A_h, B_h, fake_rp, np.concatenate(sel_col), np.concatenate(sel_val), rows, B200)
+    # the whole row_ptr against the oracle's symbolic pass (every row, exact)
+    ref_rp = oracle.symbolic(A_h, A_h, B200, threads=ORACLE_THREADS)
+    np.testing.assert_array_equal(C.row_ptr.cpu().numpy(), ref_rp)
+    # the 64 heaviest rows (uncapped) + 24 random rows per inter decile, bit-exact
+    rows = _sample_rows(inter, n_top=64, per_decile=24)
+    ref = oracle.spgemm(_rows_of(A_h, rows), A_h, B200, threads=ORACLE_THREADS)
+    _assert_rows_bitexact(C, rows, ref)
+    _record("r2_cfg3_parity", {"rows_checked": int(rows.size), "products_checked": int(inter[rows].sum()),
+                               "max_row_products": int(inter[rows].max()), "row_ptr_rows": int(A.n_rows),
+                               "nnz_c": nnz})
     # checksum of C, then linearity: (2A).B == 2(A.B) exactly (power-of-two scaling is exact;
     # B stays unscaled, so for C=A.A the second operand is the original A)
     ck = _checksum(C)
@@ -163,21 +214,41 @@ def test_cfg5_row_sample():
     assert A.row_ptr.dtype == torch.int64
     A_h = A.numpy()
     inter = _inter(A_h, A_h)
-    rows = _sample_rows(inter, n_top=0, per_decile=12, max_inter=2_000_000, seed=5)
+    # the 32 heaviest rows (2.3e8 - 3.2e8 products each; C rows ~48% dense) + 12 per decile
+    rows = _sample_rows(inter, n_top=32, per_decile=12, seed=5)
     sub = _rows_of(A_h, rows)
-    dev_sub = CsrMatrix(sub.n_rows, sub.n_cols, torch.from_numpy(sub.row_ptr).cuda(),
-                        torch.from_numpy(np.asarray(sub.col)).cuda(), torch.from_numpy(sub.val).cuda())
-    res = spgemm_magnus(dev_sub, A, sys=B200)
-    ref = oracle.spgemm(sub, A_h, B200)
+    res = spgemm_magnus(_dev(sub), A, sys=B200)
+    ref = oracle.spgemm(sub, A_h, B200, threads=min(ORACLE_THREADS, 8))
     np.testing.assert_array_equal(res.C.row_ptr.cpu().numpy(), ref.row_ptr)
     np.testing.assert_array_equal(res.C.col.cpu().numpy().view(np.uint32), ref.col)
     np.testing.assert_array_equal(res.C.val.cpu().numpy().view(np.uint64), ref.val.view(np.uint64))
-    # and the heaviest rows (too slow for the oracle): structure + determinism
-    heavy = np.argsort(inter)[-8:]
-    hs = _rows_of(A_h, np.sort(heavy))
-    dh = CsrMatrix(hs.n_rows, hs.n_cols, torch.from_numpy(hs.row_ptr).cuda(), torch.from_numpy(np.asarray(hs.col)).cuda(),
-                   torch.from_numpy(hs.val).cuda())
-    r1 = spgemm_magnus(dh, A, sys=B200)
-    _structural(r1.C, hs.n_rows, A.n_cols)
-    r2 = spgemm_magnus(dh, A, sys=B200)
-    assert torch.equal(r1.C.col, r2.C.col) and torch.equal(r1.C.val.view(torch.int64), r2.C.val.view(torch.int64))
+    _record("r2_cfg5_parity", {"rows_checked": int(rows.size), "products_checked": int(inter[rows].sum()),
+                               "max_row_products": int(inter[rows].max()), "nnz_checked": int(ref.row_ptr[-1])})
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_default_params_vs_reference_defaults(cfg):
+    """`spgemm_magnus(A, B)` (sys=None: the B200 parameters) against the reference's result under
+    its own host defaults: pattern bit-exact, values within the north-star tolerance."""
+    if cfg in (1, 2):
+        A_h, B_h = generate.make_config_cpu(cfg)
+        rows = None
+    else:
+        A, B = generate.make_config_device(cfg)
+        A_h = A.numpy()
+        B_h = A_h if B is A else B.numpy()
+        rows = _sample_rows(_inter(A_h, B_h), n_top=64, per_decile=24) if cfg == 3 else None
+    Ain = A_h if rows is None else _rows_of(A_h, rows)
+    res = spgemm_magnus(_dev(Ain) if cfg >= 3 else Ain, _dev(B_h) if cfg >= 3 else B_h)   # sys=None
+    ref = oracle.spgemm(Ain, B_h, HOST_DEFAULT, threads=ORACLE_THREADS)
+    absref = oracle.spgemm(_abs(Ain), _abs(B_h), HOST_DEFAULT, threads=ORACLE_THREADS)
+    rp = res.C.row_ptr.cpu().numpy() if torch.is_tensor(res.C.row_ptr) else res.C.row_ptr
+    col = res.C.col.cpu().numpy() if torch.is_tensor(res.C.col) else res.C.col
+    val = res.C.val.cpu().numpy() if torch.is_tensor(res.C.val) else res.C.val
+    np.testing.assert_array_equal(rp, ref.row_ptr)
+    np.testing.assert_array_equal(np.asarray(col).view(np.uint32), ref.col)
+    strict, canc, ndiff = _tolerance(val, ref.val, absref.val)
+    _record(f"r2_tolerance_cfg{cfg}", {"entries": int(ref.val.size), "entries_differing": ndiff,
+                                       "max_strict_rel": strict, "max_abs_over_sum_abs": canc,
+                                       "rows": "all" if rows is None else int(rows.size)})
+    assert canc <= 1e-12

@@ -13,8 +13,9 @@ import pytest
 torch = pytest.importorskip("torch")
 
 from oracle import oracle  # noqa: E402
-from paper_2501_07056_b200 import (AccumThresholds, CsrMatrix, OverBudgetError, SystemParams, generate,  # noqa: E402
-                                   spgemm_magnus)
+from paper_2501_07056_b200 import (AccumThresholds, ContractViolation, CsrMatrix, InputError,  # noqa: E402
+                                   OverBudgetError, SystemParams, compute_chunk_plan, generate, spgemm_magnus)
+from paper_2501_07056_b200.planner import NUMERIC, SYMBOLIC  # noqa: E402
 
 from golden_util import expected, inputs, runs, system  # noqa: E402
 
@@ -122,8 +123,8 @@ def test_edge_shapes():
     Z = CsrMatrix(0, 5, np.zeros(1, np.int64), np.empty(0, np.int32), np.empty(0))
     r = spgemm_magnus(Z, F, sys=B200)
     assert r.C.n_rows == 0 and r.C.nnz == 0
-    with pytest.raises(Exception):
-        spgemm_magnus(F, F, sys=B200)   # 5x7 . 5x7: dimension mismatch -> InputError
+    with pytest.raises(InputError):
+        spgemm_magnus(F, F, sys=B200)   # 5x7 . 5x7: dimension mismatch
 
 
 @pytest.mark.parametrize("crossover", [512, 1024, 3000])
@@ -228,3 +229,82 @@ def test_numeric_host_readback(batch_elems, monkeypatch):
     np.testing.assert_array_equal(rp.cpu().numpy(), ref.row_ptr)
     np.testing.assert_array_equal(hc.numpy().view(np.uint32), ref.col)
     np.testing.assert_array_equal(hv.numpy().view(np.uint64), ref.val.view(np.uint64))
+
+
+def _broken(kind):
+    A = generate.rmat(10, 8, seed=12)
+    rp = np.asarray(A.row_ptr, np.int64).copy()
+    col = np.asarray(A.col).astype(np.uint32).copy()
+    val = np.asarray(A.val).copy()
+    row = int(np.argmax(np.diff(rp) >= 3))
+    if kind == "b_col_range":
+        col[rp[row]] = A.n_cols + 5
+    elif kind == "dup":
+        col[rp[row] + 1] = col[rp[row]]
+    elif kind == "unsorted":
+        col[rp[row]], col[rp[row] + 1] = col[rp[row] + 1], col[rp[row]]
+    elif kind == "row_ptr":
+        rp[3] = rp[4] + 2
+    return A, CsrMatrix(A.n_rows, A.n_cols, rp, col, val)
+
+
+@pytest.mark.parametrize("kind,exc", [("b_col_range", ContractViolation), ("dup", InputError),
+                                      ("unsorted", InputError), ("row_ptr", InputError)])
+def test_input_contract_errors(kind, exc):
+    """Out-of-span B columns -> ContractViolation (magnus.py:208-209, 245-246); malformed row_ptr
+    and non-canonical rows -> InputError (validate_csr, matrix.py:119-150), checked on the device
+    before any kernel indexes through the inputs."""
+    A, bad = _broken(kind)
+    with pytest.raises(exc):
+        spgemm_magnus(A, bad, sys=B200)
+    if kind != "b_col_range":
+        with pytest.raises(InputError):
+            spgemm_magnus(bad, A, sys=B200)
+    # A column outside B's rows
+    A2 = generate.rmat(10, 8, seed=12)
+    col = np.asarray(A2.col).astype(np.uint32).copy()
+    col[7] = A2.n_cols + 1
+    with pytest.raises(InputError):
+        spgemm_magnus(CsrMatrix(A2.n_rows, A2.n_cols, A2.row_ptr, col, A2.val), A2, sys=B200)
+    # the library still works afterwards
+    assert spgemm_magnus(A, A, sys=B200).C.nnz > 0
+
+
+@pytest.mark.parametrize("sysname", ["b200", "coarse"])
+def test_phase_entry_points(sysname):
+    """magnus_symbolic / magnus_numeric / categorize_rows with the reference signatures
+    (magnus.py:68, 420, 459) give the full pipeline's result."""
+    from paper_2501_07056_b200 import categorize_rows, magnus_numeric, magnus_symbolic, row_intermediate_stats
+    sysp = {"b200": B200, "coarse": COARSE}[sysname]
+    A = generate.rmat(12, 16, seed=21)
+    th = AccumThresholds()
+    plan_s = compute_chunk_plan(sysp, A.n_cols, SYMBOLIC)
+    plan_n = compute_chunk_plan(sysp, A.n_cols, NUMERIC)
+    st = row_intermediate_stats(A, A)
+    cats = categorize_rows(st, plan_s, sysp, th)
+    ref = oracle.spgemm(A, A, sysp)
+    counts = cats.counts
+    assert [counts[k] for k in ("sort", "dense", "fine", "coarse")] == [ref.counters[k] for k in
+                                                                        ("rows_sort", "rows_dense", "rows_fine",
+                                                                         "rows_coarse")]
+    rp = magnus_symbolic(A, A, plan_s, cats, st, sysp, th)
+    np.testing.assert_array_equal(rp, ref.row_ptr)
+    res = magnus_numeric(A, A, rp, plan_n, cats, st, sysp, th)
+    assert_same(res, ref)
+    # a row_ptr from elsewhere is re-derived and checked; a wrong one is a ContractViolation
+    res2 = magnus_numeric(A, A, rp.copy(), plan_n, cats, st, sysp, th)
+    np.testing.assert_array_equal(res2.C.val.view(np.uint64), ref.val.view(np.uint64))
+    bad = rp.copy()
+    bad[5:] += 1
+    with pytest.raises(ContractViolation):
+        magnus_numeric(A, A, bad, plan_n, cats, st, sysp, th)
+
+
+def test_workspace_pool_release():
+    from paper_2501_07056_b200 import _lib
+    A = generate.rmat(13, 16, seed=2)
+    spgemm_magnus(A, A, sys=B200)
+    assert _lib.workspace_reserved() > 0
+    _lib.release_workspace()
+    assert _lib.workspace_reserved() == 0
+    assert spgemm_magnus(A, A, sys=B200).C.nnz > 0

@@ -119,12 +119,12 @@ def test_generators_are_deterministic_and_canonical():
     b = generate.rmat(10, 16, seed=7)
     np.testing.assert_array_equal(a.col, b.col)
     np.testing.assert_array_equal(a.val, b.val)
-    validate_csr(a)
+    assert validate_csr(a)
     u = generate.uniform_rows(1000, 5000, 16, seed=3)
-    validate_csr(u)
+    assert validate_csr(u)
     assert (np.diff(u.row_ptr) == 16).all()
     s = generate.stencil27(8)
-    validate_csr(s)
+    assert validate_csr(s)
     assert s.nnz == (3 * 8 - 2) ** 3
 
 
