@@ -263,6 +263,85 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
   }
 }
 
+// Direct big-chunk path (MAGNUS_BIG_PATH=direct): windows and expand units of heavy rows
+// [h0, h1), one warp per row.  Big chunks (> kBinE
+// products) are reduced straight from B by k_bd_num (big_direct.cuh): they get neither a
+// window nor a unit, units never span them, and the small chunks' slices are placed by the
+// small-chunk element prefix `cs` (k_bd_plan) -- the reorder buffer holds small-chunk
+// products only.
+__global__ void k_bin_plan_small(const int32_t* __restrict__ rows, int64_t h0, int64_t h1, const int64_t* __restrict__ mn,
+                           const int64_t* __restrict__ mx, int shift, const int64_t* __restrict__ choff,
+                           const uint32_t* __restrict__ ce, const uint32_t* __restrict__ cs,
+                           BinItem* __restrict__ wins, unsigned long long* __restrict__ nwin,
+                           BinItem* __restrict__ wins_t, BinItem* __restrict__ units,
+                           unsigned long long* __restrict__ nunit, int64_t cap_units) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long* nunit_back = nwin + 6;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t h = h0 + warp; h < h1; h += nwarps) {
+    const int64_t i = rows[h];
+    const RowBins rb = row_bins(mn[i], mx[i], shift);
+    const uint32_t* e = ce + choff[h];
+    const uint32_t* es = cs + choff[h];
+    const int ucj = kBinCur >> rb.cs;                       // chunks per unit (entries <= kBinCur)
+    bool rowbig = false;
+    for (int q0 = 0; q0 < rb.nchunk && !rowbig; q0 += 32) {
+      const int cj = q0 + lane;
+      const bool big = cj < rb.nchunk && __ldg(e + rb.je(cj)) - __ldg(e + rb.js(cj)) > (uint32_t)kBinE;
+      rowbig = __any_sync(0xffffffffu, big);
+    }
+    const bool split = rowbig || (int64_t)__ldg(es + rb.nb) > kBinUnitMax || rb.nchunk > ucj;
+    int wstart = 0, ustart = 0;
+    for (int q0 = 0; q0 < rb.nchunk; q0 += 32) {
+      const int cj = q0 + lane;
+      const bool valid = cj < rb.nchunk;
+      const int js = valid ? rb.js(cj) : 0, je = valid ? rb.je(cj) : 0;
+      const uint32_t pe = valid ? __ldg(e + js) : 0u, pi = valid ? __ldg(e + je) : 0u;
+      const uint32_t spe = valid ? __ldg(es + js) : 0u, spi = valid ? __ldg(es + je) : 0u;
+      const uint32_t n = pi - pe;
+      const bool big = valid && n > (uint32_t)kBinE;
+      // chunks above kBinWinT stand alone, so a packed window never holds more than kBinE
+      const uint32_t n_next = valid && cj + 1 < rb.nchunk ? __ldg(e + rb.je(cj + 1)) - pi : 0u;
+      const bool next_big = n_next > (uint32_t)kBinWinT;
+      const bool next_isbig = n_next > (uint32_t)kBinE;
+      // chunks of <= 32 products ("tiny") are reduced in registers by a shared-memory-free
+      // kernel: windows never mix tiny and other chunks
+      const bool tiny = n <= 32u, next_tiny = n_next <= 32u;
+      // ---- reduce windows: runs of small chunks; each sub-bin of a big chunk alone
+      // (windows also end every kBinWinT chunks: the direct reducer keeps a cursor per chunk)
+      const bool cut = valid && (cj == rb.nchunk - 1 || n > (uint32_t)kBinWinT || next_big || pe / kBinWinT != pi / kBinWinT ||
+                                 ((cj + 1) % kBinWinT) == 0 || tiny != next_tiny);
+      const uint32_t cm = __ballot_sync(0xffffffffu, cut);
+      {
+        const uint32_t prev = cm & lanemask_lt();
+        const int ws = prev ? q0 + 31 - __clz(prev) + 1 : wstart;
+        const int wjs = rb.js(ws);
+        const bool emit = cut && !big && pi > __ldg(e + wjs);
+        emit_items(emit && !tiny, BinItem{(int32_t)h, wjs, je, 0}, wins, nwin);
+        emit_items(emit && tiny, BinItem{(int32_t)h, wjs, je, 0}, wins_t, nwin + 8);
+        if (cm) wstart = q0 + 31 - __clz(cm) + 1;
+      }
+      // ---- expand units: runs of small chunks (whole chunks, so small-chunk slices stay in one
+      // unit), cut at big chunks
+      const bool ucut = valid && (cj == rb.nchunk - 1 || big || next_isbig ||
+                                  (split && (((cj + 1) % ucj) == 0 ||
+                                             (int64_t)spe / kBinUnitMax != (int64_t)spi / kBinUnitMax)));
+      const uint32_t um = __ballot_sync(0xffffffffu, ucut);
+      {
+        const uint32_t prev = um & lanemask_lt();
+        const int us = prev ? q0 + 31 - __clz(prev) + 1 : ustart;
+        const int ujs = rb.js(us);
+        const uint32_t un = spi - __ldg(es + ujs);
+        const bool uemit = ucut && !big && un > 0;
+        emit_items(uemit && un >= kUnitFront, BinItem{(int32_t)h, ujs, je, split ? 0 : 1}, units, nunit);
+        emit_items(uemit && un < kUnitFront, BinItem{(int32_t)h, ujs, je, split ? 0 : 1}, units, nunit_back, cap_units);
+        if (um) ustart = q0 + 31 - __clz(um) + 1;
+      }
+    }
+  }
+}
+
 // Expand, two-pass variant: one CTA per unit.  The unit's stream (its k segments in
 // ascending k) is split into kE2W contiguous warp ranges.  Pass 1 counts each warp's
 // products per chunk; a prefix over warps gives every warp its starting slot in every

@@ -16,6 +16,7 @@
 
 #include "../../include/magnus_b200.h"
 #include "baselines.cuh"
+#include "big_direct.cuh"
 #include "binned_rows.cuh"
 #include "microbench.cuh"
 #include "common.cuh"
@@ -168,6 +169,11 @@ struct magnus_ctx {
   int64_t* nent = nullptr;
   int64_t* hinter = nullptr;
   uint32_t* ce = nullptr;     // chunk tables: element prefix / distinct-column prefix
+  // direct big-chunk path (big_direct.cuh, MAGNUS_BIG_PATH=direct)
+  bool big_direct = false;
+  uint32_t* cs = nullptr;     // numeric phase: small-chunk element prefix (big chunks excluded)
+  int64_t* hbase_s = nullptr;   // numeric phase: exclusive prefix of the heavy rows' small-chunk products
+  std::vector<int64_t> h_small;
   uint32_t* cd = nullptr;
   uint32_t* cbm_slot = nullptr;   // per chunk entry: slot of its column bitmap in cbm_pool (big chunks)
   uint32_t* cbm_pool = nullptr;
@@ -374,6 +380,10 @@ int magnus_ctx_create(magnus_ctx** out) {
                                (int)mg::bin_big_smem(mg::kBinMaxShift, mg::kBigD)));
   MG_CUDA(cudaFuncSetAttribute(mg::k_bin_big<mg::kBigDWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::bin_big_smem(mg::kBinMaxShift, mg::kBigDWide)));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_bd_num<mg::kBigD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(mg::bd_warp_smem(mg::kBinMaxShift, mg::kBigD) * mg::kBdW)));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_bd_num<mg::kBigDWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(mg::bd_warp_smem(mg::kBinMaxShift, mg::kBigDWide) * mg::kBdW)));
   MG_CUDA(cudaFuncSetAttribute(mg::k_bin_expand2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::Exp2Smem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_heavy_sym2, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -442,7 +452,7 @@ int magnus_row_stats(const magnus_csr* A, const magnus_csr* B, int64_t* inter, i
 // B window index (direct_rows.cuh k_didx_*): for B rows of at least kDirIdxMinLen entries,
 // the position of the first column >= g << wlog for every g.  Replaces the binary searches
 // of segment bounds at window / unit boundaries by one load.
-static int setup_bidx(magnus_ctx* ctx, int wlog) {
+static int setup_bidx(magnus_ctx* ctx, int wlog, int64_t min_len_req) {
   cudaStream_t s = ctx->stream;
   const mg::DevCsr& B = ctx->B;
   ctx->dir_wlog = wlog;
@@ -461,7 +471,7 @@ static int setup_bidx(magnus_ctx* ctx, int wlog) {
   // shortest indexed row: >= kDirIdxMinLen, and the index within ~1 GB
   const int64_t cap_bytes = int64_t(1) << 30;
   int b = 0;
-  while ((int64_t(1) << b) < mg::kDirIdxMinLen) ++b;
+  while ((int64_t(1) << b) < min_len_req) ++b;
   for (;; ++b) {
     int64_t rows_ge = 0;
     for (int q = b; q < 40; ++q) rows_ge += (int64_t)hist[q];
@@ -489,7 +499,7 @@ static int setup_bidx(magnus_ctx* ctx, int wlog) {
 }
 
 static int setup_direct(magnus_ctx* ctx) {
-  int rc = setup_bidx(ctx, std::min(mg::kDirLog, (int)ctx->sem.shift_num));
+  int rc = setup_bidx(ctx, std::min(mg::kDirLog, (int)ctx->sem.shift_num), mg::kDirIdxMinLen);
   if (rc) return rc;
   const size_t smem = mg::DirSmem::kWarp * mg::kDirNW;
   MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->dir_occ, mg::k_dir_num, 32 * mg::kDirNW, smem));
@@ -759,6 +769,12 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     ctx->sym2 = ctx->binned && !(sp && std::strcmp(sp, "window") == 0) &&
                 (ctx->plan_num.plan_cols >> ctx->sem.shift_num) + 1 <= mg::kS2Chunks;
   }
+  {
+    // big chunks straight from B (big_direct.cuh) instead of through the reorder buffer:
+    // opt-in (MAGNUS_BIG_PATH=direct; bit-identical, measured slower on cfg3 -- DESIGN.md)
+    const char* bp = std::getenv("MAGNUS_BIG_PATH");
+    ctx->big_direct = ctx->binned && !ctx->direct && bp && std::strcmp(bp, "direct") == 0;
+  }
   ctx->gshift = mg::bin_shift_of(ctx->sem.shift_num);
   ctx->ncnt = ctx->binned ? (ctx->plan_num.plan_cols >> ctx->gshift) : n_chunks_global;
   const bool chunk_global = ctx->ncnt > mg::kChunkSmem;
@@ -808,7 +824,9 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     int rc2 = setup_direct(ctx);
     if (rc2) return rc2;
   } else if (ctx->binned) {
-    int rc2 = setup_bidx(ctx, ctx->gshift);   // expand units start and end on sub-bin boundaries
+    // expand units start and end on sub-bin boundaries; the direct big-chunk kernel looks up
+    // every (k, chunk) segment here: there rows down to 2 entries are indexed
+    int rc2 = setup_bidx(ctx, ctx->gshift, ctx->big_direct ? 2 : mg::kDirIdxMinLen);
     if (rc2) return rc2;
   }
   trace_point(s, "setup: B window index");
@@ -1017,6 +1035,246 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   return MAGNUS_OK;
 }
 
+// Big chunks of all heavy rows, straight from B (big_direct.cuh); also the small-chunk tables
+// (cs, per-row small totals -> ctx->h_small, ctx->hbase_s) the binned small-chunk path uses.
+static int launch_big_direct(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, double* c_val) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nH = ctx->host_stats[mg::kStatNH];
+  const int shift = ctx->sem.shift_num;
+  const int64_t nchunks = std::max<int64_t>(ctx->sem.n_chunks_num, 1);
+  unsigned long long* bucket = nullptr;   // 2 * nchunks counters + total
+  int64_t* hsmall = nullptr;
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&bucket), (size_t)(2 * nchunks + 8) * 8, s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&hsmall), (size_t)std::max<int64_t>(nH, 1) * 8, s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&ctx->cs), (size_t)std::max<int64_t>(ctx->total_ent, 1) * 4, s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&ctx->hbase_s), (size_t)(nH + 1) * 8, s));
+  MG_CUDA(cudaMemsetAsync(bucket, 0, (size_t)(2 * nchunks + 8) * 8, s));
+  const unsigned gp = (unsigned)std::min<int64_t>((nH + 7) / 8, (int64_t)ctx->sm_count * 16);
+  // items chunk-major (default) or in arrival order (MAGNUS_BD_ORDER=arrival; tuning)
+  const char* bo = std::getenv("MAGNUS_BD_ORDER");
+  const bool bd_chunk_major = !(bo && std::strcmp(bo, "arrival") == 0);
+  ctx->begin(MAGNUS_K_BIN_PLAN);
+  mg::k_bd_plan<0><<<gp, 256, 0, s>>>(ctx->listH, nH, ctx->mn, ctx->mx, shift, ctx->choff, ctx->ce, ctx->cd,
+                                      ctx->cbm_slot, c_rp, ctx->cs, hsmall, bucket, nchunks, nullptr, bd_chunk_major);
+  mg::k_bd_bucket_scan<<<1, 1024, 0, s>>>(bucket, 2 * nchunks, bucket + 2 * nchunks);
+  {
+    const int64_t tiles = (nH + mg::kScanTile - 1) / mg::kScanTile;
+    mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(hsmall, nH, ctx->tile_sums);
+    mg::k_scan_tiles<<<1, 1024, 0, s>>>(ctx->tile_sums, tiles);
+    mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(hsmall, nH, ctx->tile_sums, ctx->hbase_s);
+  }
+  ctx->end();
+  ctx->launches += 4;
+  MG_CUDA(cudaGetLastError());
+  unsigned long long tots[2] = {0, 0};   // first wide item, all items
+  ctx->h_small.resize(nH);
+  MG_CUDA(cudaMemcpyAsync(&tots[0], bucket + nchunks, 8, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaMemcpyAsync(&tots[1], bucket + 2 * nchunks, 8, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaMemcpyAsync(ctx->h_small.data(), hsmall, nH * 8, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  const uint64_t n_narrow = tots[0], n_all = tots[1];
+  if (n_all > 0) {
+    mg::BdItem* items = nullptr;
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&items), (size_t)n_all * sizeof(mg::BdItem), s));
+    int32_t* aslot = nullptr;   // B index slot per A nonzero (k_bd_aprep)
+    uint32_t* abase = nullptr;  // B row start per A nonzero
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&aslot), (size_t)std::max<int64_t>(ctx->A.nnz, 1) * 4, s));
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&abase), (size_t)std::max<int64_t>(ctx->A.nnz, 1) * 4, s));
+    mg::k_bd_aprep<<<(unsigned)std::min<int64_t>((ctx->A.nnz + 255) / 256 + 1, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+        ctx->A, ctx->B, ctx->bslot, aslot, abase);
+    ++ctx->launches;
+    ctx->begin(MAGNUS_K_BIN_PLAN);
+    mg::k_bd_plan<1><<<gp, 256, 0, s>>>(ctx->listH, nH, ctx->mn, ctx->mx, shift, ctx->choff, ctx->ce, ctx->cd,
+                                        ctx->cbm_slot, c_rp, ctx->cs, hsmall, bucket, nchunks, items, bd_chunk_major);
+    ctx->end();
+    MG_CUDA(cudaMemsetAsync(bucket + 2 * nchunks + 2, 0, 16, s));   // tickets
+    const size_t sm_n = mg::bd_warp_smem(shift, mg::kBigD) * mg::kBdW;
+    const size_t sm_w = mg::bd_warp_smem(shift, mg::kBigDWide) * mg::kBdW;
+    int occ_n = 1, occ_w = 1;
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_n, mg::k_bd_num<mg::kBigD>, 32 * mg::kBdW, sm_n));
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_w, mg::k_bd_num<mg::kBigDWide>, 32 * mg::kBdW, sm_w));
+    occ_n = std::max(occ_n, 1);
+    occ_w = std::max(occ_w, 1);
+    ctx->begin(MAGNUS_K_BIN_BIG);
+    if (n_narrow > 0)
+      mg::k_bd_num<mg::kBigD><<<(unsigned)(ctx->sm_count * occ_n), 32 * mg::kBdW, sm_n, s>>>(
+          ctx->A, ctx->B, ctx->listH, ctx->sem, items, n_narrow, bucket + 2 * nchunks + 2, ctx->cbm_pool, aslot, abase,
+          ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, c_col, c_val, ctx->err);
+    if (n_all > n_narrow)
+      mg::k_bd_num<mg::kBigDWide><<<(unsigned)(ctx->sm_count * occ_w), 32 * mg::kBdW, sm_w, s>>>(
+          ctx->A, ctx->B, ctx->listH, ctx->sem, items + n_narrow, n_all - n_narrow, bucket + 2 * nchunks + 3,
+          ctx->cbm_pool, aslot, abase, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, c_col, c_val, ctx->err);
+    ctx->end();
+    if (n_all > n_narrow) ++ctx->launches;
+    MG_CUDA(cudaGetLastError());
+#ifdef MG_BD_STATS
+    {
+      unsigned long long h[2][16];
+      MG_CUDA(cudaStreamSynchronize(s));
+      MG_CUDA(cudaMemcpyFromSymbol(h, mg::g_bd_stats, sizeof h));
+      const char* nm[9] = {"items", "k_lookups", "pieces", "subbatches", "waves", "single_waves", "products", "runs", "passes"};
+      for (int l = 0; l < 2; ++l) {
+        fprintf(stderr, "[bd] list %d:", l);
+        for (int q = 0; q < 9; ++q) fprintf(stderr, " %s=%llu", nm[q], h[l][q]);
+        fprintf(stderr, "\n");
+      }
+      unsigned long long z[2][16] = {};
+      MG_CUDA(cudaMemcpyToSymbol(mg::g_bd_stats, z, sizeof z));
+    }
+#endif
+    MG_CUDA(cudaFreeAsync(items, s));
+    MG_CUDA(cudaFreeAsync(aslot, s));
+    MG_CUDA(cudaFreeAsync(abase, s));
+  }
+  MG_CUDA(cudaFreeAsync(bucket, s));
+  MG_CUDA(cudaFreeAsync(hsmall, s));
+  return MAGNUS_OK;
+}
+
+// Heavy rows, numeric phase, direct big-chunk path: big chunks straight from B, then the small
+// chunks through the binned path in batches of rows whose small-chunk products fit the reorder buffer.
+static int launch_binned_direct(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, double* c_val) {
+  cudaStream_t s = ctx->stream;
+  const int64_t nH = ctx->host_stats[mg::kStatNH];
+  {
+    int rc = launch_big_direct(ctx, c_rp, c_col, c_val);
+    if (rc) return rc;
+  }
+  const std::vector<int64_t>& hsz = ctx->h_small;   // small-chunk products per heavy row
+  int64_t max_row = 0, total = 0;
+  for (int64_t h = 0; h < nH; ++h) {
+    max_row = std::max(max_row, hsz[h]);
+    total += hsz[h];
+  }
+  size_t free_b = 0, tot_b = 0;
+  MG_CUDA(cudaMemGetInfo(&free_b, &tot_b));
+  {
+    // memory the pool holds but does not use is available too
+    cudaMemPool_t pool = workspace_pool();
+    uint64_t reserved = 0, used = 0;
+    MG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+    MG_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+    if (reserved > used) free_b += (size_t)(reserved - used);
+  }
+  const int64_t per_elem = 10;   // u16 local column + f64 product
+  double frac = kBatchFracSerial;
+  if (const char* bf = std::getenv("MAGNUS_BATCH_FRAC")) {
+    const double v = std::atof(bf);
+    if (v > 0.0 && v < 0.9) frac = v;
+  }
+  int64_t cap = std::min<int64_t>(total, std::min<int64_t>((int64_t)(free_b * frac) / per_elem, int64_t(3) << 30));
+  if (const char* ce = std::getenv("MAGNUS_BATCH_ELEMS")) {   // testing: force many heavy-row batches
+    const long long v = std::atoll(ce);
+    if (v > 0) cap = std::min<int64_t>(cap, (int64_t)v);
+  }
+  cap = std::max<int64_t>(cap, std::max<int64_t>(max_row, 1));
+  // batches [h0, h1) and the largest chunk-table span of a batch
+  std::vector<int64_t> cuts{0};
+  int64_t acc = 0, ent = 0, max_ent = 0;
+  for (int64_t h = 0; h < nH; ++h) {
+    if (acc + hsz[h] > cap && h > cuts.back()) {
+      cuts.push_back(h);
+      max_ent = std::max(max_ent, ent);
+      acc = ent = 0;
+    }
+    acc += hsz[h];
+    ent += ctx->h_nent[h];
+  }
+  cuts.push_back(nH);
+  max_ent = std::max(max_ent, ent);
+  int64_t buf_elems = 0;
+  std::vector<int64_t> hb(cuts.size());
+  {
+    int64_t a = 0;
+    size_t b = 0;
+    for (int64_t h = 0; h <= nH; ++h) {
+      while (b < cuts.size() && cuts[b] == h) hb[b++] = a;
+      if (h < nH) a += hsz[h];
+    }
+    for (size_t q = 0; q + 1 < cuts.size(); ++q) buf_elems = std::max(buf_elems, hb[q + 1] - hb[q]);
+  }
+  void *bcol = nullptr, *bval = nullptr, *items = nullptr, *cnts = nullptr;
+  MG_CUDA(mg_malloc_async(&bcol, (size_t)std::max<int64_t>(buf_elems, 1) * 2 + 64, s));
+  MG_CUDA(mg_malloc_async(&bval, (size_t)std::max<int64_t>(buf_elems, 1) * 8 + 64, s));
+  // windows and units: <= one per chunk entry each
+  MG_CUDA(mg_malloc_async(&items, (size_t)std::max<int64_t>(max_ent, 1) * 3 * sizeof(mg::BinItem), s));
+  MG_CUDA(mg_malloc_async(&cnts, 128, s));
+  const size_t red_smem = mg::bin_reduce_warp_smem(ctx->sem.shift_num) * (mg::kBinT / 32);
+  int occ = 1;
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mg::k_bin_reduce, mg::kBinT, red_smem));
+  occ = std::max(occ, 1);
+  int occ_e2 = 1;
+  MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_e2, mg::k_bin_expand2, mg::kE2T, mg::Exp2Smem::kTotal));
+  occ_e2 = std::max(occ_e2, 1);
+  uint32_t* e2scr = nullptr;   // per-CTA segment tables of units with more than kE2K k's
+  const int64_t e2_stride = ((ctx->host_stats[mg::kStatMaxNk] + 8 + 3) / 4) * 4;
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&e2scr), (size_t)ctx->sm_count * occ_e2 * 5 * e2_stride * 4, s));
+  // host readback: C offset of each batch's end row (the next batch's first heavy row)
+  std::vector<int64_t> batch_end(cuts.size(), -1);
+  if (ctx->host_col) {
+    for (size_t b = 0; b + 2 < cuts.size(); ++b)
+      MG_CUDA(cudaMemcpyAsync(&batch_end[b], c_rp + ctx->h_rows[cuts[b + 1]], 8, cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+  }
+  const int64_t me = std::max<int64_t>(max_ent, 1);
+  for (size_t b = 0; b + 1 < cuts.size(); ++b) {
+    const int64_t h0 = cuts[b], h1 = cuts[b + 1];
+    if (hb[b + 1] == hb[b]) continue;   // no small-chunk products in this batch
+    mg::BinItem* wins = static_cast<mg::BinItem*>(items);
+    mg::BinItem* units = wins + me;
+    mg::BinItem* wins_t = units + me;   // windows of tiny chunks (k_bin_reduce_tiny)
+    auto* nwin = static_cast<unsigned long long*>(cnts);
+    auto* nunit = nwin + 1;
+    MG_CUDA(cudaMemsetAsync(cnts, 0, 128, s));
+    ctx->begin(MAGNUS_K_BIN_PLAN);
+    mg::k_bin_plan_small<<<(unsigned)std::min<int64_t>((h1 - h0 + 7) / 8, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+        ctx->listH, h0, h1, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->cs, wins, nwin, wins_t, units,
+        nunit, me);
+    ctx->end();
+    ctx->begin(MAGNUS_K_BIN_EXPAND);
+    mg::k_bin_expand2<<<(unsigned)(ctx->sm_count * occ_e2), mg::kE2T, mg::Exp2Smem::kTotal, s>>>(
+        ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->cs, ctx->hbase_s, hb[b], units,
+        nunit, nwin + 3, me, static_cast<uint16_t*>(bcol), static_cast<double*>(bval), ctx->bslot, ctx->bidx,
+        ctx->dir_nwin1, ctx->dir_wlog, e2scr, e2_stride, ctx->err);
+    ctx->end();
+    ctx->begin(MAGNUS_K_BIN_REDUCE);
+    mg::k_bin_reduce<<<(unsigned)(ctx->sm_count * occ), mg::kBinT, red_smem, s>>>(
+        ctx->listH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->cs, ctx->cd, ctx->hbase_s, hb[b], wins, nwin,
+        nwin + 4, static_cast<const uint16_t*>(bcol), static_cast<const double*>(bval), c_rp, c_col, c_val, ctx->err);
+    mg::k_bin_reduce_tiny<<<(unsigned)(ctx->sm_count * 8), 256, 0, s>>>(
+        ctx->listH, ctx->cat, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->cs, ctx->cd, ctx->hbase_s, hb[b], wins_t,
+        nwin + 8, nwin + 9, static_cast<const uint16_t*>(bcol), static_cast<const double*>(bval), c_rp, c_col, c_val,
+        ctx->err);
+    ctx->end();
+    ++ctx->launches;
+    MG_CUDA(cudaGetLastError());
+    if (ctx->host_col) {
+      // rows below the next batch's first heavy row are complete (light rows and big chunks
+      // ran first): read that prefix of C back on the copy stream while the next batch computes
+      const int64_t end = b + 2 < cuts.size() ? batch_end[b] : -1;
+      if (end > ctx->host_done) {
+        MG_CUDA(cudaEventRecord(ctx->ev_fork, s));
+        MG_CUDA(cudaStreamWaitEvent(ctx->aux3, ctx->ev_fork, 0));
+        MG_CUDA(cudaMemcpyAsync(ctx->host_col + ctx->host_done, c_col + ctx->host_done, (end - ctx->host_done) * 4,
+                                cudaMemcpyDeviceToHost, ctx->aux3));
+        MG_CUDA(cudaMemcpyAsync(ctx->host_val + ctx->host_done, c_val + ctx->host_done, (end - ctx->host_done) * 8,
+                                cudaMemcpyDeviceToHost, ctx->aux3));
+        ctx->host_done = end;
+      }
+    }
+  }
+  MG_CUDA(cudaFreeAsync(e2scr, s));
+  MG_CUDA(cudaFreeAsync(bcol, s));
+  MG_CUDA(cudaFreeAsync(bval, s));
+  MG_CUDA(cudaFreeAsync(items, s));
+  MG_CUDA(cudaFreeAsync(cnts, s));
+  MG_CUDA(cudaFreeAsync(ctx->cs, s));
+  MG_CUDA(cudaFreeAsync(ctx->hbase_s, s));
+  ctx->cs = nullptr;
+  ctx->hbase_s = nullptr;
+  return MAGNUS_OK;
+}
+
 static int launch_light(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint32_t* c_col, double* c_val);
 
 static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint32_t* c_col, double* c_val) {
@@ -1040,7 +1298,7 @@ static int launch_rows(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint3
     int rc = launch_direct(ctx, c_rp, c_col, c_val);
     if (rc) return rc;
   } else if (nH > 0 && numeric && ctx->binned) {
-    int rc = launch_binned(ctx, c_rp, c_col, c_val);
+    int rc = ctx->big_direct ? launch_binned_direct(ctx, c_rp, c_col, c_val) : launch_binned(ctx, c_rp, c_col, c_val);
     if (rc) return rc;
   } else if (nH > 0) {
     MG_CUDA(cudaMemsetAsync(ctx->work, 0, 24, s));

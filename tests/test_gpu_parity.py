@@ -308,3 +308,22 @@ def test_workspace_pool_release():
     _lib.release_workspace()
     assert _lib.workspace_reserved() == 0
     assert spgemm_magnus(A, A, sys=B200).C.nnz > 0
+
+
+@pytest.mark.parametrize("case", ["rmat14", "hub", "hot", "rmat15"])
+@pytest.mark.parametrize("sysname", ["b200", "fine4k"])
+def test_direct_big_chunk_path(case, sysname, monkeypatch):
+    """Big chunks straight from B (MAGNUS_BIG_PATH=direct, big_direct.cuh: no reorder buffer for
+    them; the small chunks' buffer holds small-chunk products only) give the reference's bits."""
+    monkeypatch.setenv("MAGNUS_BIG_PATH", "direct")
+    if case == "hot":
+        A, B = _hot_chunk_matrix()
+    elif case == "rmat15":
+        A = B = generate.rmat(15, 16, seed=7)
+    else:
+        A, B = CASES[case]()
+    sysp = {"b200": B200, "fine4k": FINE4K}[sysname]
+    ref = oracle.spgemm(A, B, sysp)
+    assert_same(spgemm_magnus(A, B, sys=sysp), ref)
+    monkeypatch.setenv("MAGNUS_BATCH_ELEMS", "20000")   # many small-chunk batches
+    assert_same(spgemm_magnus(A, B, sys=sysp), ref)
