@@ -174,6 +174,11 @@ struct magnus_ctx {
   uint32_t* cs = nullptr;     // numeric phase: small-chunk element prefix (big chunks excluded)
   int64_t* hbase_s = nullptr;   // numeric phase: exclusive prefix of the heavy rows' small-chunk products
   std::vector<int64_t> h_small;
+  // fused warp rows (k_rows_warp Mode 2 in the symbolic pass, k_rows_copy in the numeric pass)
+  bool fused = false;
+  int64_t* fused_ub = nullptr;
+  uint32_t* fused_col = nullptr;
+  double* fused_val = nullptr;
   uint32_t* cd = nullptr;
   uint32_t* cbm_slot = nullptr;   // per chunk entry: slot of its column bitmap in cbm_pool (big chunks)
   uint32_t* cbm_pool = nullptr;
@@ -198,6 +203,7 @@ struct magnus_ctx {
   cudaStream_t aux = nullptr, aux2 = nullptr, aux3 = nullptr;   // concurrent pipelines
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_e[2] = {nullptr, nullptr}, ev_r[2] = {nullptr, nullptr}, ev_b[2] = {nullptr, nullptr};
+  cudaEvent_t ev_pl[2] = {nullptr, nullptr}, ev_it[2] = {nullptr, nullptr};   // batch plan done / plan consumed
   int64_t host_stats[mg::kStatLen] = {0};
   int64_t coarse_batches = 0;
   mg::Sem sem{};
@@ -245,6 +251,41 @@ struct magnus_ctx {
   void free_all() {
     for (void* p : allocs) cudaFreeAsync(p, stream);
     allocs.clear();
+  }
+  // B-derived state (validation, skip list, window index) kept across setups with the same B:
+  // the row waves of one product (waves.py) re-run setup per block of A against one B
+  std::vector<void*> b_allocs;
+  struct BKey {
+    const void* rp = nullptr;
+    const void* col = nullptr;
+    const void* val = nullptr;
+    int64_t n_rows = -1, n_cols = -1, nnz = -1;
+    int32_t rp_bytes = 0;
+    bool operator==(const BKey& o) const {
+      return rp == o.rp && col == o.col && val == o.val && n_rows == o.n_rows && n_cols == o.n_cols && nnz == o.nnz &&
+             rp_bytes == o.rp_bytes;
+    }
+  } bkey;
+  bool b_validated = false;
+  int bidx_wlog = -1;
+  int64_t bidx_minreq = -1;
+  void free_b() {
+    for (void* p : b_allocs) cudaFreeAsync(p, stream);
+    b_allocs.clear();
+    b_validated = false;
+    bidx_wlog = -1;
+    bidx_minreq = -1;
+    skip = nullptr;
+    bslot = nullptr;
+    bidx = nullptr;
+  }
+  template <class T>
+  cudaError_t balloc(T** p, size_t count) {
+    void* q = nullptr;
+    cudaError_t e = mg_malloc_async(&q, std::max<size_t>(count, 1) * sizeof(T), stream);
+    if (e == cudaSuccess) b_allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return e;
   }
   template <class T>
   cudaError_t alloc(T** p, size_t count) {
@@ -409,6 +450,8 @@ int magnus_ctx_create(magnus_ctx** out) {
     MG_CUDA(cudaEventCreateWithFlags(&c->ev_e[q], cudaEventDisableTiming));
     MG_CUDA(cudaEventCreateWithFlags(&c->ev_r[q], cudaEventDisableTiming));
     MG_CUDA(cudaEventCreateWithFlags(&c->ev_b[q], cudaEventDisableTiming));
+    MG_CUDA(cudaEventCreateWithFlags(&c->ev_pl[q], cudaEventDisableTiming));
+    MG_CUDA(cudaEventCreateWithFlags(&c->ev_it[q], cudaEventDisableTiming));
   }
   *out = c;
   return MAGNUS_OK;
@@ -417,6 +460,7 @@ int magnus_ctx_create(magnus_ctx** out) {
 void magnus_ctx_destroy(magnus_ctx* ctx) {
   if (!ctx) return;
   ctx->free_all();
+  ctx->free_b();
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (auto& m : ctx->marks) { cudaEventDestroy(m.a); cudaEventDestroy(m.b); }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
@@ -427,6 +471,8 @@ void magnus_ctx_destroy(magnus_ctx* ctx) {
     if (ctx->ev_e[q]) cudaEventDestroy(ctx->ev_e[q]);
     if (ctx->ev_r[q]) cudaEventDestroy(ctx->ev_r[q]);
     if (ctx->ev_b[q]) cudaEventDestroy(ctx->ev_b[q]);
+    if (ctx->ev_pl[q]) cudaEventDestroy(ctx->ev_pl[q]);
+    if (ctx->ev_it[q]) cudaEventDestroy(ctx->ev_it[q]);
   }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
@@ -441,9 +487,14 @@ int magnus_row_stats(const magnus_csr* A, const magnus_csr* B, int64_t* inter, i
   int dev = 0, sms = 148;
   MG_CUDA(cudaGetDevice(&dev));
   MG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t warps = std::min<int64_t>(A->n_rows, (int64_t)sms * 64);
-  mg::k_row_stats<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(dev_csr(*A), dev_csr(*B), inter,
-                                                                                         min_col, max_col);
+  // four rows per warp when A's rows are short (<= 12 nonzeros on average)
+  const bool short_rows = A->nnz <= 12 * A->n_rows;
+  const int64_t lanes = std::min<int64_t>(A->n_rows * (short_rows ? 8 : 32), (int64_t)sms * 64 * 32);
+  const unsigned grid = (unsigned)((lanes + 255) / 256);
+  if (short_rows)
+    mg::k_row_stats<8><<<grid, 256, 0, (cudaStream_t)stream>>>(dev_csr(*A), dev_csr(*B), inter, min_col, max_col);
+  else
+    mg::k_row_stats<32><<<grid, 256, 0, (cudaStream_t)stream>>>(dev_csr(*A), dev_csr(*B), inter, min_col, max_col);
   MG_CUDA(cudaGetLastError());
   return MAGNUS_OK;
 }
@@ -455,6 +506,18 @@ int magnus_row_stats(const magnus_csr* A, const magnus_csr* B, int64_t* inter, i
 static int setup_bidx(magnus_ctx* ctx, int wlog, int64_t min_len_req) {
   cudaStream_t s = ctx->stream;
   const mg::DevCsr& B = ctx->B;
+  if (ctx->bidx && ctx->bidx_wlog == wlog && ctx->bidx_minreq == min_len_req) return MAGNUS_OK;   // same B
+  if (ctx->bidx) {   // same B, other granularity: rebuild
+    for (void* q : {static_cast<void*>(ctx->bslot), static_cast<void*>(ctx->bidx)}) {
+      auto it = std::find(ctx->b_allocs.begin(), ctx->b_allocs.end(), q);
+      if (it != ctx->b_allocs.end()) ctx->b_allocs.erase(it);
+      MG_CUDA(cudaFreeAsync(q, s));
+    }
+    ctx->bslot = nullptr;
+    ctx->bidx = nullptr;
+  }
+  ctx->bidx_wlog = wlog;
+  ctx->bidx_minreq = min_len_req;
   ctx->dir_wlog = wlog;
   const int64_t W = int64_t(1) << ctx->dir_wlog;
   ctx->dir_nwin1 = (std::max<int64_t>(B.n_cols, 1) + W - 1) / W + 1;
@@ -478,7 +541,7 @@ static int setup_bidx(magnus_ctx* ctx, int wlog, int64_t min_len_req) {
     if (rows_ge * ctx->dir_nwin1 * 4 <= cap_bytes || b >= 39) break;
   }
   ctx->dir_min_len = int64_t(1) << b;
-  MG_CUDA(ctx->alloc(&ctx->bslot, B.n_rows + 1));
+  MG_CUDA(ctx->balloc(&ctx->bslot, B.n_rows + 1));
   ctx->begin(MAGNUS_K_DIR_INDEX);
   mg::k_didx_slots<<<g, 256, 0, s>>>(B, ctx->dir_min_len, ctx->bslot, dbuf + 40);
   ctx->end();
@@ -486,7 +549,7 @@ static int setup_bidx(magnus_ctx* ctx, int wlog, int64_t min_len_req) {
   MG_CUDA(cudaMemcpyAsync(&nidx, dbuf + 40, 8, cudaMemcpyDeviceToHost, s));
   MG_CUDA(cudaStreamSynchronize(s));
   ctx->dir_nidx = (int64_t)nidx;
-  MG_CUDA(ctx->alloc(&ctx->bidx, (size_t)std::max<int64_t>(1, ctx->dir_nidx) * ctx->dir_nwin1));
+  MG_CUDA(ctx->balloc(&ctx->bidx, (size_t)std::max<int64_t>(1, ctx->dir_nidx) * ctx->dir_nwin1));
   if (nidx > 0) {
     ctx->begin(MAGNUS_K_DIR_INDEX);
     mg::k_didx_fill<<<(unsigned)std::min<int64_t>(((int64_t)nidx * 32 + 255) / 256, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
@@ -546,15 +609,19 @@ static int launch_direct(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
 static int validate_inputs(magnus_ctx* ctx, const magnus_csr& A, const magnus_csr& B, cudaStream_t s) {
   const bool same = A.row_ptr == B.row_ptr && A.col == B.col && A.n_rows == B.n_rows;
   auto launch = [&](const magnus_csr& m, unsigned long long* f) {
-    const int64_t warps = std::max<int64_t>(1, std::min<int64_t>(m.n_rows, (int64_t)ctx->sm_count * 64));
-    mg::k_validate<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(dev_csr(m), f);
+    const bool short_rows = m.nnz <= 12 * m.n_rows;   // four rows per warp
+    const int64_t lanes =
+        std::max<int64_t>(32, std::min<int64_t>(m.n_rows * (short_rows ? 8 : 32), (int64_t)ctx->sm_count * 64 * 32));
+    const unsigned grid = (unsigned)((lanes + 255) / 256);
+    if (short_rows) mg::k_validate<8><<<grid, 256, 0, s>>>(dev_csr(m), f);
+    else mg::k_validate<32><<<grid, 256, 0, s>>>(dev_csr(m), f);
     ++ctx->launches;
   };
   unsigned long long* fb = nullptr;
   MG_CUDA(ctx->alloc(&fb, 2));
   MG_CUDA(cudaMemsetAsync(fb, 0, 16, s));
   launch(A, fb);
-  if (!same) launch(B, fb + 1);
+  if (!same && !ctx->b_validated) launch(B, fb + 1);
   MG_CUDA(cudaGetLastError());
   unsigned long long h[2] = {0, 0};
   MG_CUDA(cudaMemcpyAsync(h, fb, 16, cudaMemcpyDeviceToHost, s));
@@ -573,6 +640,7 @@ static int validate_inputs(magnus_ctx* ctx, const magnus_csr& A, const magnus_cs
   if (h[1] & 2) return set_err(MAGNUS_CONTRACT, "column index outside the planned fine-level span (B column >= n_cols)");
   if (h[0] & 4) return set_err(MAGNUS_INPUT, bad("A", 4));
   if (h[1] & 4) return set_err(MAGNUS_INPUT, bad("B", 4));
+  ctx->b_validated = true;
   return MAGNUS_OK;
 }
 
@@ -596,11 +664,28 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   // per-setup allocations are gone: no pointer may survive into this setup
   ctx->cbm_slot = ctx->cbm_pool = nullptr;
   ctx->cbm_cap = 0;
-  ctx->bslot = nullptr;
-  ctx->bidx = nullptr;
   ctx->kst = nullptr;
+  {
+    magnus_ctx::BKey k;
+    k.rp = B->row_ptr;
+    k.col = B->col;
+    k.val = B->val;
+    k.n_rows = B->n_rows;
+    k.n_cols = B->n_cols;
+    k.nnz = B->nnz;
+    k.rp_bytes = B->rp_bytes;
+    if (!(k == ctx->bkey)) {
+      ctx->stream = (cudaStream_t)stream;
+      ctx->free_b();
+      ctx->bkey = k;
+    }
+  }
   ctx->ce = ctx->cd = nullptr;
   ctx->direct = ctx->binned = false;
+  ctx->fused = false;
+  ctx->fused_ub = nullptr;
+  ctx->fused_col = nullptr;
+  ctx->fused_val = nullptr;
   ctx->stream = (cudaStream_t)stream;
   cudaStream_t s = ctx->stream;
   ctx->A = dev_csr(*A);
@@ -635,18 +720,18 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     int rc0 = validate_inputs(ctx, *A, *B, s);
     if (rc0) return rc0;
   }
-  {
+  if (!ctx->skip) {
     const int64_t nskip = (B->nnz + 31) / 32;
-    MG_CUDA(ctx->alloc(&ctx->skip, nskip + 1));
+    MG_CUDA(ctx->balloc(&ctx->skip, nskip + 1));
     if (nskip > 0) {
       mg::k_build_skip<<<(unsigned)std::min<int64_t>((nskip + 255) / 256, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
           B->col, B->nnz, ctx->skip);
       MG_CUDA(cudaGetLastError());
       ++ctx->launches;
     }
-    ctx->B.skip = ctx->skip;
-    if (A->row_ptr == B->row_ptr && A->col == B->col) ctx->A.skip = ctx->skip;
   }
+  ctx->B.skip = ctx->skip;
+  if (A->row_ptr == B->row_ptr && A->col == B->col) ctx->A.skip = ctx->skip;
   if (n > 0) {
     ctx->begin(MAGNUS_K_ROW_STATS);
     rc = magnus_row_stats(A, B, ctx->inter, ctx->mn, ctx->mx, stream);
@@ -905,6 +990,8 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   }
   // two buffer sets when the expand of batch b+1 overlaps the reducers of batch b
   const int nbuf = (cuts.size() > 2 && !serial) ? 2 : 1;
+  // two plan sets: batch b+1 is planned on a side stream while batch b computes
+  const int nitem = cuts.size() > 2 ? 2 : 1;
   const int64_t max_big = std::max<int64_t>(max_ent, 1) + buf_elems / mg::kBigSplit + 1;
   void *bcol[2] = {nullptr, nullptr}, *bval[2] = {nullptr, nullptr}, *items[2] = {nullptr, nullptr},
        *cnts[2] = {nullptr, nullptr};
@@ -912,6 +999,8 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     // (+64 bytes: bulk copies read 16-byte aligned supersets of a slice)
     MG_CUDA(mg_malloc_async(&bcol[q], (size_t)std::max<int64_t>(buf_elems, 1) * 2 + 64, s));
     MG_CUDA(mg_malloc_async(&bval[q], (size_t)std::max<int64_t>(buf_elems, 1) * 8 + 64, s));
+  }
+  for (int q = 0; q < nitem; ++q) {
     // windows and units: <= one per chunk entry; big-chunk parts: <= entries + elements / kBigSplit
     MG_CUDA(mg_malloc_async(&items[q], (size_t)std::max<int64_t>(max_ent, 1) * 3 * sizeof(mg::BinItem) +
                                            (size_t)max_big * 2 * sizeof(mg::BigItem), s));
@@ -952,14 +1041,31 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   cudaStream_t sr = ctx->aux, sbig = ctx->aux2;
   if (serial) sr = sbig = s;
   bool used[2] = {false, false};
+  // plan of batch b into plan set b % nitem, on stream st
+  auto plan_batch = [&](size_t b, cudaStream_t st) {
+    const int qi = (int)(b % nitem);
+    const int64_t h0 = cuts[b], h1 = cuts[b + 1];
+    mg::BinItem* wins = static_cast<mg::BinItem*>(items[qi]);
+    mg::BinItem* units = wins + std::max<int64_t>(max_ent, 1);
+    mg::BinItem* wins_t = units + std::max<int64_t>(max_ent, 1);
+    mg::BigItem* bigs = reinterpret_cast<mg::BigItem*>(wins_t + std::max<int64_t>(max_ent, 1));
+    auto* nwin = static_cast<unsigned long long*>(cnts[qi]);
+    cudaMemsetAsync(cnts[qi], 0, 128, st);
+    cudaEvent_t m0 = ctx->begin_on(MAGNUS_K_BIN_PLAN, st);
+    mg::k_bin_plan<<<(unsigned)std::min<int64_t>((h1 - h0 + 7) / 8, (int64_t)ctx->sm_count * 16), 256, 0, st>>>(
+        ctx->listH, h0, h1, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, wins, nwin, wins_t, bigs, nwin + 2,
+        units, nwin + 1, std::max<int64_t>(max_ent, 1), max_big, ctx->cd, ctx->hbase, hb[b], c_rp, ctx->cbm_slot);
+    ctx->end_on(MAGNUS_K_BIN_PLAN, m0, st);
+  };
+  plan_batch(0, s);
   for (size_t b = 0; b + 1 < cuts.size(); ++b) {
     const int q = (int)(b % nbuf);
-    const int64_t h0 = cuts[b], h1 = cuts[b + 1];
-    mg::BinItem* wins = static_cast<mg::BinItem*>(items[q]);
+    const int qi = (int)(b % nitem);
+    mg::BinItem* wins = static_cast<mg::BinItem*>(items[qi]);
     mg::BinItem* units = wins + std::max<int64_t>(max_ent, 1);
     mg::BinItem* wins_t = units + std::max<int64_t>(max_ent, 1);   // windows of tiny chunks (k_bin_reduce_tiny)
     mg::BigItem* bigs = reinterpret_cast<mg::BigItem*>(wins_t + std::max<int64_t>(max_ent, 1));
-    auto* nwin = static_cast<unsigned long long*>(cnts[q]);
+    auto* nwin = static_cast<unsigned long long*>(cnts[qi]);
     auto* nunit = nwin + 1;
     auto* nbig = nwin + 2;
     if (used[q]) {   // the reducers of batch b - nbuf still read this buffer set
@@ -967,12 +1073,14 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
       MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_b[q], 0));
     }
     used[q] = true;
-    MG_CUDA(cudaMemsetAsync(cnts[q], 0, 128, s));
-    ctx->begin(MAGNUS_K_BIN_PLAN);
-    mg::k_bin_plan<<<(unsigned)std::min<int64_t>((h1 - h0 + 7) / 8, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
-        ctx->listH, h0, h1, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, wins, nwin, wins_t, bigs, nbig, units,
-        nunit, std::max<int64_t>(max_ent, 1), max_big, ctx->cd, ctx->hbase, hb[b], c_rp, ctx->cbm_slot);
-    ctx->end();
+    if (b > 0) MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_pl[qi], 0));   // this batch's plan (side stream)
+    if (b + 2 < cuts.size()) {
+      // plan batch b+1 beside this batch, once batch b-1 (the previous user of that set) is done
+      const int qn = (int)((b + 1) % nitem);
+      if (b > 0) MG_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_it[qn], 0));
+      plan_batch(b + 1, ctx->aux);
+      MG_CUDA(cudaEventRecord(ctx->ev_pl[qn], ctx->aux));
+    }
     ctx->begin(MAGNUS_K_BIN_EXPAND);
     mg::k_bin_expand2<<<(unsigned)(ctx->sm_count * occ_e2), mg::kE2T, mg::Exp2Smem::kTotal, s>>>(
         ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
@@ -1004,6 +1112,9 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
         nwin + 9, static_cast<const uint16_t*>(bcol[q]), static_cast<const double*>(bval[q]), c_rp, c_col, c_val, ctx->err);
     ctx->end_on(MAGNUS_K_BIN_REDUCE, m3, sr);
     MG_CUDA(cudaEventRecord(ctx->ev_r[q], sr));
+    MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_b[q], 0));
+    MG_CUDA(cudaStreamWaitEvent(s, ctx->ev_r[q], 0));
+    MG_CUDA(cudaEventRecord(ctx->ev_it[qi], s));   // plan set qi free again
     MG_CUDA(cudaGetLastError());
     if (ctx->host_col && sr == s && sbig == s) {
       // rows below the next batch's first heavy row are complete (light rows ran first):
@@ -1029,6 +1140,8 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   for (int q = 0; q < nbuf; ++q) {
     MG_CUDA(cudaFreeAsync(bcol[q], s));
     MG_CUDA(cudaFreeAsync(bval[q], s));
+  }
+  for (int q = 0; q < nitem; ++q) {
     MG_CUDA(cudaFreeAsync(items[q], s));
     MG_CUDA(cudaFreeAsync(cnts[q], s));
   }
@@ -1360,13 +1473,57 @@ static int launch_light(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint
   if (nW > 0) {
     const int64_t blocks = (nW + mg::kWT / 32 - 1) / (mg::kWT / 32);
     const unsigned grid = (unsigned)std::min<int64_t>(blocks, (int64_t)ctx->sm_count * 8);
+    const bool key32 = ctx->B.n_cols <= (int64_t(1) << 24);
+    if (!numeric) {
+      // fused warp rows: the symbolic pass also computes the values, into the rows' upper-bound
+      // slots of a buffer (<= 256 products per row); the numeric pass copies them into C.
+      // Used when that buffer fits a quarter of the free HBM (MAGNUS_FUSED_ROWS=0 disables it).
+      ctx->fused = false;
+      const char* fe = std::getenv("MAGNUS_FUSED_ROWS");
+      if (!(fe && std::strcmp(fe, "0") == 0)) {
+        MG_CUDA(ctx->alloc(&ctx->fused_ub, nW + 1));
+        mg::k_gather_inter<<<(unsigned)std::min<int64_t>((nW + 255) / 256, (int64_t)ctx->sm_count * 8), 256, 0, s>>>(
+            ctx->listW, nW, ctx->inter, ctx->fused_ub);
+        int64_t* ts = nullptr;
+        const int64_t tiles = (nW + mg::kScanTile - 1) / mg::kScanTile;
+        MG_CUDA(ctx->alloc(&ts, tiles + 1));
+        mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->fused_ub, nW, ts);
+        mg::k_scan_tiles<<<1, 1024, 0, s>>>(ts, tiles);
+        mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(ctx->fused_ub, nW, ts, ctx->fused_ub);
+        ctx->launches += 4;
+        int64_t tot = 0;
+        MG_CUDA(cudaMemcpyAsync(&tot, ctx->fused_ub + nW, 8, cudaMemcpyDeviceToHost, s));
+        MG_CUDA(cudaStreamSynchronize(s));
+        size_t fr = 0, to = 0;
+        MG_CUDA(cudaMemGetInfo(&fr, &to));
+        if ((size_t)tot * 12 <= fr / 4) {
+          MG_CUDA(ctx->alloc(&ctx->fused_col, tot));
+          MG_CUDA(ctx->alloc(&ctx->fused_val, tot));
+          ctx->fused = true;
+        }
+      }
+    }
     ctx->begin(numeric ? MAGNUS_K_NUM_WARP : MAGNUS_K_SYM_WARP);
-    if (numeric)
-      mg::k_rows_warp<true><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts, c_rp,
-                                                      c_col, c_val, ctx->err);
+    if (numeric && ctx->fused)
+      mg::k_rows_copy<<<grid, 256, 0, s>>>(ctx->listW, nW, ctx->fused_ub, ctx->fused_col, ctx->fused_val, c_rp, c_col, c_val);
+    else if (numeric && key32)
+      mg::k_rows_warp<1, true><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts,
+                                                         c_rp, c_col, c_val, ctx->err);
+    else if (numeric)
+      mg::k_rows_warp<1, false><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts,
+                                                          c_rp, c_col, c_val, ctx->err);
+    else if (ctx->fused && key32)
+      mg::k_rows_warp<2, true><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts,
+                                                         nullptr, ctx->fused_col, ctx->fused_val, ctx->err, ctx->fused_ub);
+    else if (ctx->fused)
+      mg::k_rows_warp<2, false><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts,
+                                                          nullptr, ctx->fused_col, ctx->fused_val, ctx->err, ctx->fused_ub);
+    else if (key32)
+      mg::k_rows_warp<0, true><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts,
+                                                         c_rp, c_col, c_val, ctx->err);
     else
-      mg::k_rows_warp<false><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts,
-                                                       c_rp, c_col, c_val, ctx->err);
+      mg::k_rows_warp<0, false><<<grid, mg::kWT, 0, s>>>(ctx->A, ctx->B, ctx->listW, nW, ctx->cat, ctx->sem, ctx->counts,
+                                                          c_rp, c_col, c_val, ctx->err);
     ctx->end();
     MG_CUDA(cudaGetLastError());
   }

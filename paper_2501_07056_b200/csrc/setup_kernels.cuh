@@ -4,18 +4,23 @@
 
 namespace mg {
 
-// row_intermediate_stats (reference gustavson.py:97-134): one warp per row.
-// inter[i] = sum of nnz(B_k) over k in A_i; [min_col, max_col] spans the first /
-// last column of every referenced non-empty B row; empty product -> (0, 0, -1).
+// row_intermediate_stats (reference gustavson.py:97-134): a group of G lanes per row (G = 32,
+// or 8 for matrices with short rows: four rows per warp).  inter[i] = sum of nnz(B_k) over k
+// in A_i; [min_col, max_col] spans the first / last column of every referenced non-empty B
+// row; empty product -> (0, 0, -1).
+template <int G>
 __global__ void k_row_stats(DevCsr A, DevCsr B, int64_t* __restrict__ inter, int64_t* __restrict__ mn,
                             int64_t* __restrict__ mx) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < A.n_rows; i += nwarps) {
-    const int64_t a0 = A.rp(i), a1 = A.rp(i + 1);
+  const int gl = threadIdx.x & (G - 1);
+  const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+  const int64_t iters = (A.n_rows + ngrp - 1) / ngrp;   // every lane runs the same trip count (shuffles)
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t i = grp + it * ngrp;
+    const bool row = i < A.n_rows;
+    const int64_t a0 = row ? A.rp(i) : 0, a1 = row ? A.rp(i + 1) : 0;
     int64_t s = 0, lo = INT64_MAX, hi = -1;
-    for (int64_t t = a0 + lane; t < a1; t += 32) {
+    for (int64_t t = a0 + gl; t < a1; t += G) {
       const int64_t k = __ldg(A.col + t);
       const int64_t b0 = B.rp(k), b1 = B.rp(k + 1);
       s += b1 - b0;
@@ -26,13 +31,13 @@ __global__ void k_row_stats(DevCsr A, DevCsr B, int64_t* __restrict__ inter, int
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = G / 2; o > 0; o >>= 1) {
       s += __shfl_xor_sync(0xffffffffu, s, o);
       int64_t l2 = __shfl_xor_sync(0xffffffffu, lo, o), h2 = __shfl_xor_sync(0xffffffffu, hi, o);
       lo = l2 < lo ? l2 : lo;
       hi = h2 > hi ? h2 : hi;
     }
-    if (lane == 0) {
+    if (gl == 0 && row) {
       inter[i] = s;
       mn[i] = s > 0 ? lo : 0;
       mx[i] = s > 0 ? hi : -1;
@@ -46,22 +51,23 @@ __global__ void k_row_stats(DevCsr A, DevCsr B, int64_t* __restrict__ inter, int
 // adjacent pairs (coalesced).  flags: 1 = row_ptr not monotone / row_ptr[0] != 0 /
 // row_ptr[n] != nnz, 2 = column >= n_cols, 4 = columns not strictly increasing in a row
 // (unsorted or duplicate columns: the device kernels require canonical rows).
+template <int G>
 __global__ void k_validate(DevCsr M, unsigned long long* __restrict__ flags) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31, gl = threadIdx.x & (G - 1);
+  const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
   const uint64_t ncols = (uint64_t)M.n_cols;
   unsigned f = 0;
-  if (warp == 0 && lane == 0) {
+  if (grp == 0 && gl == 0) {
     if (M.rp(0) != 0 || M.rp(M.n_rows) != M.nnz) f |= 1u;
   }
-  for (int64_t i = warp; i < M.n_rows; i += nwarps) {
+  for (int64_t i = grp; i < M.n_rows; i += ngrp) {
     const int64_t a0 = M.rp(i), a1 = M.rp(i + 1);
     if (a1 < a0 || a0 < 0 || a1 > M.nnz) {
       f |= 1u;
       continue;
     }
-    for (int64_t t = a0 + lane; t < a1; t += 32) {
+    for (int64_t t = a0 + gl; t < a1; t += G) {
       const uint32_t c = __ldg(M.col + t);
       if ((uint64_t)c >= ncols) f |= 2u;
       if (t + 1 < a1 && __ldg(M.col + t + 1) <= c) f |= 4u;

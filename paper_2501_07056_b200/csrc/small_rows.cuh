@@ -5,6 +5,8 @@
 // reference gives it (see Sem / mode_of).  Warp-per-row up to 256 elements,
 // CTA-per-row up to 4096.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace mg {
@@ -63,16 +65,19 @@ __device__ __forceinline__ bool seq_mode(int cat, const Sem& sem, const F& chunk
 // repeats (the common case: the product of two random sparse rows) -- writes C directly:
 // a single contribution is x0 under the sort association and +0.0 + x0 under the dense one.
 // Returns 0 when a column repeats: the sorted keys and the values are then left in shared
-// memory for the general path.
-template <bool Numeric>
+// memory for the general path.  Mode: 0 count only, 1 values to C, 2 values to the
+// row's upper-bound slot of the fused buffer and the count (k_rows_warp).  K: u32 keys
+// (column << 8 | position) when columns < 2^24, else u64.
+template <int Mode, class K>
 __device__ __forceinline__ int reg_row64(const DevCsr& B, int64_t b0, uint32_t inc, uint32_t len, double av, uint32_t nn,
                                          unsigned long long* keys, double* vals, int ci, const Sem& sem,
                                          int64_t* __restrict__ counts, int64_t i, int64_t out0, int64_t out1,
                                          uint32_t* __restrict__ c_col, double* __restrict__ c_val,
                                          unsigned long long* __restrict__ err) {
+  constexpr bool Numeric = Mode != 0;
   const int lane = threadIdx.x & 31;
   const uint32_t off = inc - len;
-  unsigned long long k0, k1;
+  K k0, k1;
   double v0 = 0.0, v1 = 0.0;
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
@@ -86,11 +91,11 @@ __device__ __forceinline__ int reg_row64(const DevCsr& B, int64_t b0, uint32_t i
     const int64_t bb = __shfl_sync(0xffffffffu, b0, lo);
     const uint32_t oo = __shfl_sync(0xffffffffu, off, lo);
     const double a = __shfl_sync(0xffffffffu, av, lo);
-    unsigned long long key = ~0ull;
+    K key = ~K(0);
     double v = 0.0;
     if (q < nn) {
       const int64_t pp = bb + (q - oo);
-      key = ((unsigned long long)__ldg(B.col + pp) << 8) | q;
+      key = ((K)__ldg(B.col + pp) << 8) | (K)q;
       if (Numeric) v = __dmul_rn(a, __ldg(B.val + pp));
     }
     if (r == 0) { k0 = key; v0 = v; } else { k1 = key; v1 = v; }
@@ -101,23 +106,24 @@ __device__ __forceinline__ int reg_row64(const DevCsr& B, int64_t b0, uint32_t i
 #pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
       if (j == 32) {
-        const unsigned long long lo = k0 < k1 ? k0 : k1, hi = k0 < k1 ? k1 : k0;
+        const K lo = k0 < k1 ? k0 : k1, hi = k0 < k1 ? k1 : k0;
         k0 = lo;
         k1 = hi;
       } else {
-        const unsigned long long p0 = __shfl_xor_sync(0xffffffffu, k0, j), p1 = __shfl_xor_sync(0xffffffffu, k1, j);
+        const K p0 = __shfl_xor_sync(0xffffffffu, k0, j), p1 = __shfl_xor_sync(0xffffffffu, k1, j);
         const bool lower = (lane & j) == 0;
         const bool up0 = (lane & k) == 0 || k == 64, up1 = ((lane + 32) & k) == 0 || k == 64;
-        const bool t0 = lower ? (up0 ? p0 < k0 : p0 > k0) : (up0 ? p0 > k0 : p0 < k0);
-        const bool t1 = lower ? (up1 ? p1 < k1 : p1 > k1) : (up1 ? p1 > k1 : p1 < k1);
+        // take the partner when it belongs here: (lower == up) wants the smaller
+        const bool t0 = (lower == up0) ? p0 < k0 : p0 > k0;
+        const bool t1 = (lower == up1) ? p1 < k1 : p1 > k1;
         if (t0) k0 = p0;
         if (t1) k1 = p1;
       }
     }
   }
-  const unsigned long long c0 = k0 >> 8, c1 = k1 >> 8;
-  const unsigned long long pc0 = __shfl_up_sync(0xffffffffu, c0, 1), pc1 = __shfl_up_sync(0xffffffffu, c1, 1);
-  const unsigned long long last0 = __shfl_sync(0xffffffffu, c0, 31);
+  const K c0 = k0 >> 8, c1 = k1 >> 8;
+  const K pc0 = __shfl_up_sync(0xffffffffu, c0, 1), pc1 = __shfl_up_sync(0xffffffffu, c1, 1);
+  const K last0 = __shfl_sync(0xffffffffu, c0, 31);
   const bool ok0 = (uint32_t)lane < nn, ok1 = (uint32_t)(lane + 32) < nn;
   const bool h0 = ok0 && (lane == 0 || pc0 != c0);
   const bool h1 = ok1 && (lane == 0 ? last0 != c1 : pc1 != c1);
@@ -151,12 +157,13 @@ __device__ __forceinline__ int reg_row64(const DevCsr& B, int64_t b0, uint32_t i
         c_col[out0 + 32 + lane] = (uint32_t)c1;
         c_val[out0 + 32 + lane] = x1;
       }
+      if (Mode == 2 && lane == 0) counts[i] = distinct;
       return 1;
     }
   }
-  // general path: sorted keys and the values (by position) to shared memory
-  keys[lane] = k0;
-  keys[lane + 32] = k1;
+  // general path: sorted keys (as u64 column << 8 | position) and the values (by position)
+  keys[lane] = k0 == ~K(0) ? ~0ull : (unsigned long long)k0;
+  keys[lane + 32] = k1 == ~K(0) ? ~0ull : (unsigned long long)k1;
   vals[lane] = v0;
   vals[lane + 32] = v1;
   return 0;
@@ -166,11 +173,18 @@ __device__ __forceinline__ int reg_row64(const DevCsr& B, int64_t b0, uint32_t i
 constexpr int kWT = 256;  // threads per block (8 warps, one row each)
 constexpr int kWSlots = 256;
 
-template <bool Numeric>
+// Mode 0: distinct counts (symbolic); 1: values into C at c_rp (numeric); 2: fused -- values
+// into the row's slot of a buffer laid out by the rows' upper bounds (ub: exclusive prefix of
+// the listed rows' product counts) and the counts; the numeric pass then only copies
+// (k_rows_copy).  Key32: columns < 2^24 (32-bit sort keys).
+template <int Mode, bool Key32 = false>
 __global__ void __launch_bounds__(kWT) k_rows_warp(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, int64_t nrows,
                                                    const int8_t* __restrict__ cat, Sem sem, int64_t* __restrict__ counts,
                                                    const int64_t* __restrict__ c_rp, uint32_t* __restrict__ c_col,
-                                                   double* __restrict__ c_val, unsigned long long* __restrict__ err) {
+                                                   double* __restrict__ c_val, unsigned long long* __restrict__ err,
+                                                   const int64_t* __restrict__ ub = nullptr) {
+  constexpr bool Numeric = Mode != 0;
+  using K = typename std::conditional<Key32, uint32_t, unsigned long long>::type;
   // per warp: keys (u64) + vals (f64)
   __shared__ unsigned long long s_keys[kWT / 32][kWSlots];
   __shared__ double s_vals[kWT / 32][kWSlots];
@@ -199,8 +213,10 @@ __global__ void __launch_bounds__(kWT) k_rows_warp(DevCsr A, DevCsr B, const int
       const uint32_t inc = warp_incl_scan(len);
       const uint32_t nn = __shfl_sync(0xffffffffu, inc, 31);
       if (nn <= 64u) {
-        const int st = reg_row64<Numeric>(B, b0, inc, len, av, nn, keys, vals, cat[i], sem, counts, i,
-                                           Numeric ? c_rp[i] : 0, Numeric ? c_rp[i + 1] : 0, c_col, c_val, err);
+        const int64_t o0 = Mode == 1 ? c_rp[i] : (Mode == 2 ? ub[w] : 0);
+        const int64_t o1 = Mode == 1 ? c_rp[i + 1] : (Mode == 2 ? ub[w + 1] : 0);
+        const int st = reg_row64<Mode, K>(B, b0, inc, len, av, nn, keys, vals, cat[i], sem, counts, i, o0, o1, c_col,
+                                          c_val, err);
         if (st) continue;   // done in registers (else: keys / vals sorted in shared memory)
         if (lane == 0) s_n[wib] = (int)nn;
         goto heads;
@@ -243,8 +259,8 @@ __global__ void __launch_bounds__(kWT) k_rows_warp(DevCsr A, DevCsr B, const int
     // column heads, ranks
     int rank_base = 0;
     const int ci = Numeric ? (int)cat[i] : 0;
-    const int64_t out0 = Numeric ? c_rp[i] : 0;
-    const int64_t out_n = Numeric ? c_rp[i + 1] - out0 : 0;
+    const int64_t out0 = Mode == 1 ? c_rp[i] : (Mode == 2 ? ub[w] : 0);
+    const int64_t out_n = Mode == 1 ? c_rp[i + 1] - out0 : (Mode == 2 ? ub[w + 1] - out0 : 0);
     for (int p0 = 0; p0 < n; p0 += 32) {
       const int p = p0 + lane;
       bool head = false;
@@ -280,7 +296,7 @@ __global__ void __launch_bounds__(kWT) k_rows_warp(DevCsr A, DevCsr B, const int
       rank_base += __popc(m);
     }
     if (lane == 0) {
-      if (Numeric) {
+      if (Mode == 1) {
         if (rank_base != out_n) atomicOr(err, 1ull);
       } else {
         counts[i] = rank_base;
@@ -288,6 +304,32 @@ __global__ void __launch_bounds__(kWT) k_rows_warp(DevCsr A, DevCsr B, const int
     }
     __syncwarp();
   }
+}
+
+// Numeric pass of fused rows: row w of the list moves from its upper-bound slot (ub[w]) of the
+// fused buffer to C (one warp per row, <= 256 entries, coalesced).
+__global__ void __launch_bounds__(256) k_rows_copy(const int32_t* __restrict__ rows, int64_t nrows,
+                                                   const int64_t* __restrict__ ub, const uint32_t* __restrict__ f_col,
+                                                   const double* __restrict__ f_val, const int64_t* __restrict__ c_rp,
+                                                   uint32_t* __restrict__ c_col, double* __restrict__ c_val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp; w < nrows; w += nwarps) {
+    const int64_t i = rows[w];
+    const int64_t d0 = c_rp[i], n = c_rp[i + 1] - d0, s0 = ub[w];
+    for (int64_t t = lane; t < n; t += 32) {
+      c_col[d0 + t] = __ldg(f_col + s0 + t);
+      c_val[d0 + t] = __ldg(f_val + s0 + t);
+    }
+  }
+}
+
+// ub[w] = inter[rows[w]] (then scanned into the fused buffer's row slots)
+__global__ void k_gather_inter(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __restrict__ inter,
+                               int64_t* __restrict__ out) {
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nrows; w += (int64_t)gridDim.x * blockDim.x)
+    out[w] = inter[rows[w]];
 }
 
 // ================================================================ CTA per row

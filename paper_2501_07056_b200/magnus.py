@@ -139,6 +139,19 @@ class MagnusPlan:
         self.row_ptr = None
         self.nnz = None
 
+    def reset(self, A) -> None:
+        """Re-plan for another A (same B, parameters and stream) on the same context: the
+        B-derived device state (validation, skip list, window index) is kept.  Used by the
+        row waves of products whose C cannot be held at once (waves.py)."""
+        _check_dims(A, self.B)
+        self.A = _to_device(A, self.device)
+        self._a = _abi(self.A)
+        th = _lib.Thresholds(self.thresholds.sort_dense_crossover, self.thresholds.sort_sweet_spot)
+        _lib.check(_lib.lib().magnus_setup(self.ctx.h, C.byref(self._a), C.byref(self._b), C.byref(_sys_abi(self.sys)),
+                                           C.byref(th), int(self.force_fine_only), C.c_void_p(self.stream.cuda_stream)))
+        self.row_ptr = None
+        self.nnz = None
+
     def categories(self) -> RowCategories:
         torch = _torch()
         cat = torch.empty(self.A.n_rows, dtype=torch.int8, device=self.device)
