@@ -96,6 +96,15 @@ int magnus_row_stats(const magnus_csr* A, const magnus_csr* B, int64_t* inter, i
 /* Per-row categories (int8, MAGNUS_CAT_*) computed by the last magnus_setup; copies n_rows bytes to device dst. */
 int magnus_categories(magnus_ctx* ctx, int8_t* dst, void* stream);
 
+/* Caller-owned workspace.  After magnus_symbolic: the device bytes the numeric
+ * phase's largest buffer -- the heavy rows' reorder buffer (u16 column + f64 product per heavy-row
+ * product) -- takes in one batch (*preferred) and at least (*minimum: the heaviest row); 0 when
+ * the call has no heavy rows.  magnus_set_workspace(ctx, ws, bytes): the next magnus_numeric carves
+ * that buffer from the caller's device memory (>= *minimum bytes; batches are sized to it) instead
+ * of the library pool; (NULL, 0) returns to library-owned workspace. */
+int magnus_workspace_bytes(magnus_ctx* ctx, int64_t* preferred, int64_t* minimum);
+int magnus_set_workspace(magnus_ctx* ctx, void* ws, int64_t bytes);
+
 /* The library's device workspace (chunk tables, reorder buffers, per-call scratch) comes from a
  * private stream-ordered memory pool of the current device, never from the default pool.  Freed
  * workspace stays reserved there between calls; magnus_release_workspace() synchronises the

@@ -76,7 +76,7 @@ EXPORTS = ["magnus_compute_chunk_plan", "magnus_ctx_create", "magnus_ctx_destroy
            "magnus_numeric_host", "magnus_gd_scratch_bytes", "magnus_gd_symbolic", "magnus_gd_numeric",
            "magnus_esc_expand", "magnus_esc_compress", "magnus_mb_histogram", "magnus_mb_reorder_scratch_bytes",
            "magnus_mb_reorder", "magnus_mb_dense", "magnus_mb_stream",
-           "magnus_mb_scan_scratch_bytes", "magnus_mb_scan", "magnus_release_workspace", "magnus_workspace_reserved"]
+           "magnus_mb_scan_scratch_bytes", "magnus_mb_scan", "magnus_release_workspace", "magnus_workspace_reserved", "magnus_workspace_bytes", "magnus_set_workspace"]
 KERNEL_NAMES = ["row_stats", "categorize", "sym_warp", "sym_block", "sym_heavy", "scan", "num_warp", "num_block",
                 "num_heavy", "sym_dense", "num_dense", "bin_plan", "bin_expand", "bin_reduce", "bin_big", "dir_index",
                 "dir_plan", "dir_num"]
@@ -135,6 +135,8 @@ def lib():
         L.magnus_mb_scan.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]
         L.magnus_mb_stream.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         L.magnus_release_workspace.argtypes = []
+        L.magnus_workspace_bytes.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.magnus_set_workspace.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
         L.magnus_workspace_reserved.argtypes = []
         L.magnus_workspace_reserved.restype = C.c_int64
         _LIB = L

@@ -174,6 +174,9 @@ struct magnus_ctx {
   uint32_t* cs = nullptr;     // numeric phase: small-chunk element prefix (big chunks excluded)
   int64_t* hbase_s = nullptr;   // numeric phase: exclusive prefix of the heavy rows' small-chunk products
   std::vector<int64_t> h_small;
+  // caller-owned workspace for the heavy rows' reorder buffer (magnus_set_workspace)
+  unsigned char* ws_ptr = nullptr;
+  int64_t ws_bytes = 0;
   // fused warp rows (k_rows_warp Mode 2 in the symbolic pass, k_rows_copy in the numeric pass)
   bool fused = false;
   int64_t* fused_ub = nullptr;
@@ -302,6 +305,28 @@ extern "C" {
 const char* magnus_last_error(void) { return g_err.c_str(); }
 const char* magnus_version(void) { return "magnus_b200 0.1 (sm_100a)"; }
 int64_t magnus_launch_count(magnus_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int magnus_workspace_bytes(magnus_ctx* ctx, int64_t* preferred, int64_t* minimum) {
+  if (!ctx || !preferred || !minimum) return set_err(MAGNUS_INPUT, "null argument");
+  if (!ctx->ready || !ctx->have_symbolic) return set_err(MAGNUS_CONTRACT, "magnus_workspace_bytes needs magnus_symbolic first");
+  int64_t total = 0, max_row = 0;
+  if (ctx->binned && !ctx->direct && !ctx->big_direct)
+    for (int64_t h : ctx->h_hinter) {
+      total += h;
+      max_row = std::max(max_row, h);
+    }
+  *preferred = total ? total * 10 + 256 : 0;   // one batch: u16 column + f64 product per heavy-row product
+  *minimum = max_row ? max_row * 10 + 256 : 0;
+  return MAGNUS_OK;
+}
+
+int magnus_set_workspace(magnus_ctx* ctx, void* ws, int64_t bytes) {
+  if (!ctx) return set_err(MAGNUS_INPUT, "null argument");
+  if ((ws == nullptr) != (bytes == 0) || bytes < 0) return set_err(MAGNUS_INPUT, "workspace pointer and size disagree");
+  ctx->ws_ptr = static_cast<unsigned char*>(ws);
+  ctx->ws_bytes = bytes;
+  return MAGNUS_OK;
+}
 
 int magnus_release_workspace(void) {
   cudaMemPool_t pool = workspace_pool();
@@ -965,6 +990,14 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
     const long long v = std::atoll(ce);
     if (v > 0) cap = std::min<int64_t>(cap, (int64_t)v);
   }
+  const bool own_ws = ctx->ws_ptr != nullptr && serial;   // caller-owned reorder buffer
+  if (own_ws) {
+    const int64_t ws_cap = (ctx->ws_bytes - 256) / per_elem;
+    if (ws_cap < max_row)
+      return set_err(MAGNUS_INPUT, "workspace of " + std::to_string(ctx->ws_bytes) + " bytes is below the minimum " +
+                                       std::to_string(max_row * per_elem + 256) + " (magnus_workspace_bytes)");
+    cap = std::min(total, ws_cap);
+  }
   cap = std::max(cap, max_row);
   // batches [h0, h1) and the largest chunk-table span of a batch
   std::vector<int64_t> cuts{0};
@@ -997,6 +1030,12 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
        *cnts[2] = {nullptr, nullptr};
   for (int q = 0; q < nbuf; ++q) {
     // (+64 bytes: bulk copies read 16-byte aligned supersets of a slice)
+    if (own_ws) {   // values first (16-byte aligned), then the columns; 64 bytes slack each
+      const uintptr_t base = (reinterpret_cast<uintptr_t>(ctx->ws_ptr) + 15) & ~uintptr_t(15);
+      bval[q] = reinterpret_cast<void*>(base);
+      bcol[q] = reinterpret_cast<void*>((base + (size_t)std::max<int64_t>(buf_elems, 1) * 8 + 64 + 15) & ~uintptr_t(15));
+      continue;
+    }
     MG_CUDA(mg_malloc_async(&bcol[q], (size_t)std::max<int64_t>(buf_elems, 1) * 2 + 64, s));
     MG_CUDA(mg_malloc_async(&bval[q], (size_t)std::max<int64_t>(buf_elems, 1) * 8 + 64, s));
   }
@@ -1138,6 +1177,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   }
   MG_CUDA(cudaFreeAsync(e2scr, s));
   for (int q = 0; q < nbuf; ++q) {
+    if (own_ws) continue;
     MG_CUDA(cudaFreeAsync(bcol[q], s));
     MG_CUDA(cudaFreeAsync(bval[q], s));
   }

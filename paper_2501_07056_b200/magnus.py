@@ -169,10 +169,30 @@ class MagnusPlan:
         self.row_ptr, self.nnz = rp, int(nnz.value)
         return rp
 
-    def numeric(self, row_ptr=None, out=None, host_out=None):
+    def workspace_bytes(self):
+        """(preferred, minimum) device bytes of the numeric phase's reorder buffer (after symbolic)."""
+        pref, mini = C.c_int64(0), C.c_int64(0)
+        _lib.check(_lib.lib().magnus_workspace_bytes(self.ctx.h, C.byref(pref), C.byref(mini)))
+        return int(pref.value), int(mini.value)
+
+    def numeric(self, row_ptr=None, out=None, host_out=None, workspace=None):
         """magnus_numeric (reference magnus.py:459-542): fills C; returns (C, counters).
         host_out=(col, val): host tensors (page-locked for overlap) that receive C's col / val;
-        completed row ranges are read back while later row batches compute."""
+        completed row ranges are read back while later row batches compute.
+        workspace: a caller-owned device tensor (>= workspace_bytes()[1] bytes) that holds the
+        heavy rows' reorder buffer instead of the library's pool."""
+        if workspace is not None:
+            if not workspace.is_cuda:
+                raise InputError("workspace must be a device tensor")
+            nbytes = workspace.numel() * workspace.element_size()
+            _lib.check(_lib.lib().magnus_set_workspace(self.ctx.h, C.c_void_p(workspace.data_ptr()), C.c_int64(nbytes)))
+        try:
+            return self._numeric(row_ptr, out, host_out)
+        finally:
+            if workspace is not None:
+                _lib.lib().magnus_set_workspace(self.ctx.h, None, C.c_int64(0))
+
+    def _numeric(self, row_ptr=None, out=None, host_out=None):
         torch = _torch()
         rp = self.row_ptr if row_ptr is None else row_ptr
         if rp is None or rp is not self.row_ptr:

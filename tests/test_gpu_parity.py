@@ -327,3 +327,29 @@ def test_direct_big_chunk_path(case, sysname, monkeypatch):
     assert_same(spgemm_magnus(A, B, sys=sysp), ref)
     monkeypatch.setenv("MAGNUS_BATCH_ELEMS", "20000")   # many small-chunk batches
     assert_same(spgemm_magnus(A, B, sys=sysp), ref)
+
+
+def test_caller_owned_workspace():
+    """magnus_workspace_bytes / magnus_set_workspace: the reorder buffer in caller
+    memory -- at the minimum size (many batches) and at the preferred one -- gives the same bits."""
+    from paper_2501_07056_b200 import MagnusPlan
+    A = generate.rmat(14, 16, seed=31)
+    ref = oracle.spgemm(A, A, B200)
+    dev = torch.device("cuda")
+    Ad = CsrMatrix(A.n_rows, A.n_cols, torch.from_numpy(A.row_ptr).to(dev), torch.from_numpy(A.col).to(dev),
+                   torch.from_numpy(A.val).to(dev))
+    for which in (1, 0):
+        plan = MagnusPlan(Ad, Ad, sys=B200)
+        rp = plan.symbolic()
+        pref, mini = plan.workspace_bytes()
+        assert 0 < mini <= pref
+        ws = torch.empty((pref, mini)[which], dtype=torch.uint8, device=dev)
+        C, _ = plan.numeric(rp, workspace=ws)
+        plan.close()
+        np.testing.assert_array_equal(C.col.cpu().numpy().view(np.uint32), ref.col)
+        np.testing.assert_array_equal(C.val.cpu().numpy().view(np.uint64), ref.val.view(np.uint64))
+    plan = MagnusPlan(Ad, Ad, sys=B200)
+    rp = plan.symbolic()
+    with pytest.raises(InputError):
+        plan.numeric(rp, workspace=torch.empty(16, dtype=torch.uint8, device=dev))
+    plan.close()
