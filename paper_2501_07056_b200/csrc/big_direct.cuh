@@ -38,7 +38,7 @@ __global__ void k_bd_plan(const int32_t* __restrict__ rows, int64_t nH, const in
                           const uint32_t* __restrict__ cbm_slot, const int64_t* __restrict__ c_rp,
                           uint32_t* __restrict__ cs, int64_t* __restrict__ hsmall,
                           unsigned long long* __restrict__ bucket, int64_t n_chunks, BdItem* __restrict__ items,
-                          bool chunk_major) {
+                          bool chunk_major, bool no_split = false) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -60,7 +60,7 @@ __global__ void k_bd_plan(const int32_t* __restrict__ rows, int64_t nH, const in
         carry += __shfl_sync(0xffffffffu, inc, 31);
       }
       if (big) {
-        const uint32_t parts = min((uint32_t)kBigMaxParts, (n + kBigSplit - 1) / kBigSplit);
+        const uint32_t parts = no_split ? 1u : min((uint32_t)kBigMaxParts, (n + kBigSplit - 1) / kBigSplit);
         const int64_t chunk = rb.c0 + j;   // global chunk id
         const uint32_t mm = __ldg(d + j + 1) - __ldg(d + j);
         // two chunk-major lists: <= kBigD distinct columns (1024-rank accumulators) and wider

@@ -17,6 +17,7 @@
 #include "../../include/magnus_b200.h"
 #include "baselines.cuh"
 #include "big_direct.cuh"
+#include "fused_big.cuh"
 #include "binned_rows.cuh"
 #include "microbench.cuh"
 #include "common.cuh"
@@ -171,6 +172,7 @@ struct magnus_ctx {
   uint32_t* ce = nullptr;     // chunk tables: element prefix / distinct-column prefix
   // direct big-chunk path (big_direct.cuh, MAGNUS_BIG_PATH=direct)
   bool big_direct = false;
+  bool big_fused = false;     // big chunks by k_fu_big (fused_big.cuh, MAGNUS_BIG_PATH=fused)
   uint32_t* cs = nullptr;     // numeric phase: small-chunk element prefix (big chunks excluded)
   int64_t* hbase_s = nullptr;   // numeric phase: exclusive prefix of the heavy rows' small-chunk products
   std::vector<int64_t> h_small;
@@ -450,6 +452,7 @@ int magnus_ctx_create(magnus_ctx** out) {
                                (int)(mg::bd_warp_smem(mg::kBinMaxShift, mg::kBigD) * mg::kBdW)));
   MG_CUDA(cudaFuncSetAttribute(mg::k_bd_num<mg::kBigDWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)(mg::bd_warp_smem(mg::kBinMaxShift, mg::kBigDWide) * mg::kBdW)));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_fu_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mg::FuSmem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_bin_expand2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::Exp2Smem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_heavy_sym2, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -883,7 +886,9 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     // big chunks straight from B (big_direct.cuh) instead of through the reorder buffer:
     // opt-in (MAGNUS_BIG_PATH=direct; bit-identical, measured slower on cfg3 -- DESIGN.md)
     const char* bp = std::getenv("MAGNUS_BIG_PATH");
-    ctx->big_direct = ctx->binned && !ctx->direct && bp && std::strcmp(bp, "direct") == 0;
+    const bool want_fused = bp && std::strcmp(bp, "fused") == 0;
+    ctx->big_fused = ctx->binned && !ctx->direct && want_fused && ctx->sem.shift_num <= mg::kFuMaxShift;
+    ctx->big_direct = ctx->binned && !ctx->direct && ((bp && std::strcmp(bp, "direct") == 0) || ctx->big_fused);
   }
   ctx->gshift = mg::bin_shift_of(ctx->sem.shift_num);
   ctx->ncnt = ctx->binned ? (ctx->plan_num.plan_cols >> ctx->gshift) : n_chunks_global;
@@ -936,7 +941,7 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
   } else if (ctx->binned) {
     // expand units start and end on sub-bin boundaries; the direct big-chunk kernel looks up
     // every (k, chunk) segment here: there rows down to 2 entries are indexed
-    int rc2 = setup_bidx(ctx, ctx->gshift, ctx->big_direct ? 2 : mg::kDirIdxMinLen);
+    int rc2 = setup_bidx(ctx, ctx->gshift, ctx->big_direct && !ctx->big_fused ? 2 : mg::kDirIdxMinLen);
     if (rc2) return rc2;
   }
   trace_point(s, "setup: B window index");
@@ -1208,7 +1213,7 @@ static int launch_big_direct(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_c
   const bool bd_chunk_major = !(bo && std::strcmp(bo, "arrival") == 0);
   ctx->begin(MAGNUS_K_BIN_PLAN);
   mg::k_bd_plan<0><<<gp, 256, 0, s>>>(ctx->listH, nH, ctx->mn, ctx->mx, shift, ctx->choff, ctx->ce, ctx->cd,
-                                      ctx->cbm_slot, c_rp, ctx->cs, hsmall, bucket, nchunks, nullptr, bd_chunk_major);
+                                      ctx->cbm_slot, c_rp, ctx->cs, hsmall, bucket, nchunks, nullptr, bd_chunk_major, ctx->big_fused);
   mg::k_bd_bucket_scan<<<1, 1024, 0, s>>>(bucket, 2 * nchunks, bucket + 2 * nchunks);
   {
     const int64_t tiles = (nH + mg::kScanTile - 1) / mg::kScanTile;
@@ -1233,14 +1238,52 @@ static int launch_big_direct(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_c
     uint32_t* abase = nullptr;  // B row start per A nonzero
     MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&aslot), (size_t)std::max<int64_t>(ctx->A.nnz, 1) * 4, s));
     MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&abase), (size_t)std::max<int64_t>(ctx->A.nnz, 1) * 4, s));
-    mg::k_bd_aprep<<<(unsigned)std::min<int64_t>((ctx->A.nnz + 255) / 256 + 1, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
-        ctx->A, ctx->B, ctx->bslot, aslot, abase);
+    if (ctx->big_fused) {
+      mg::k_fu_aprep<<<(unsigned)std::min<int64_t>((ctx->A.nnz + 255) / 256 + 1, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+          ctx->A, ctx->B, ctx->bslot, aslot, abase);
+    } else {
+      mg::k_bd_aprep<<<(unsigned)std::min<int64_t>((ctx->A.nnz + 255) / 256 + 1, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(
+          ctx->A, ctx->B, ctx->bslot, aslot, abase);
+    }
     ++ctx->launches;
     ctx->begin(MAGNUS_K_BIN_PLAN);
     mg::k_bd_plan<1><<<gp, 256, 0, s>>>(ctx->listH, nH, ctx->mn, ctx->mx, shift, ctx->choff, ctx->ce, ctx->cd,
-                                        ctx->cbm_slot, c_rp, ctx->cs, hsmall, bucket, nchunks, items, bd_chunk_major);
+                                        ctx->cbm_slot, c_rp, ctx->cs, hsmall, bucket, nchunks, items, bd_chunk_major,
+                                        ctx->big_fused);
     ctx->end();
     MG_CUDA(cudaMemsetAsync(bucket + 2 * nchunks + 2, 0, 16, s));   // tickets
+    if (ctx->big_fused) {
+      int occ_f = 1;
+      MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_f, mg::k_fu_sweep, mg::kFuT, mg::FuSmem::kTotal));
+      occ_f = std::max(occ_f, 1);
+      const unsigned grid_f = (unsigned)(ctx->sm_count * occ_f);
+      // units: chunk ranges of ~kFuUnit big-chunk products
+      int64_t tot_inter = 0;
+      for (int64_t h = 0; h < nH; ++h) tot_inter += ctx->h_hinter[h];
+      const int64_t cap_u = nH + tot_inter / mg::kFuUnit + 1;
+      mg::BinItem* units = nullptr;
+      unsigned long long* ucnt = nullptr;
+      uint32_t* gst = nullptr;
+      const int64_t maxnk = ctx->host_stats[mg::kStatMaxNk];
+      const int64_t gst_stride = maxnk > mg::kFuKS ? ((maxnk + 31) / 32) * 32 : 0;
+      MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&units), (size_t)cap_u * sizeof(mg::BinItem), s));
+      MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&ucnt), 64, s));
+      MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&gst), std::max<size_t>((size_t)grid_f * gst_stride * 2 * 4, 16), s));
+      MG_CUDA(cudaMemsetAsync(ucnt, 0, 64, s));
+      ctx->begin(MAGNUS_K_BIN_PLAN);
+      mg::k_fu_plan<<<gp, 256, 0, s>>>(ctx->listH, nH, ctx->mn, ctx->mx, shift, ctx->choff, ctx->ce, units, ucnt, cap_u);
+      ctx->end();
+      ctx->begin(MAGNUS_K_BIN_BIG);
+      mg::k_fu_sweep<<<grid_f, mg::kFuT, mg::FuSmem::kTotal, s>>>(
+          ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem, ctx->choff, ctx->ce, ctx->cd, ctx->cbm_slot, ctx->cbm_pool,
+          units, ucnt, cap_u, ucnt + 2, aslot, abase, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, gst, gst_stride, c_rp, c_col,
+          c_val, ctx->err);
+      ctx->end();
+      MG_CUDA(cudaGetLastError());
+      MG_CUDA(cudaFreeAsync(units, s));
+      MG_CUDA(cudaFreeAsync(ucnt, s));
+      MG_CUDA(cudaFreeAsync(gst, s));
+    } else {
     const size_t sm_n = mg::bd_warp_smem(shift, mg::kBigD) * mg::kBdW;
     const size_t sm_w = mg::bd_warp_smem(shift, mg::kBigDWide) * mg::kBdW;
     int occ_n = 1, occ_w = 1;
@@ -1260,6 +1303,7 @@ static int launch_big_direct(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_c
     ctx->end();
     if (n_all > n_narrow) ++ctx->launches;
     MG_CUDA(cudaGetLastError());
+    }
 #ifdef MG_BD_STATS
     {
       unsigned long long h[2][16];

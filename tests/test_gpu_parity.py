@@ -312,10 +312,12 @@ def test_workspace_pool_release():
 
 @pytest.mark.parametrize("case", ["rmat14", "hub", "hot", "rmat15"])
 @pytest.mark.parametrize("sysname", ["b200", "fine4k"])
-def test_direct_big_chunk_path(case, sysname, monkeypatch):
-    """Big chunks straight from B (MAGNUS_BIG_PATH=direct, big_direct.cuh: no reorder buffer for
-    them; the small chunks' buffer holds small-chunk products only) give the reference's bits."""
-    monkeypatch.setenv("MAGNUS_BIG_PATH", "direct")
+@pytest.mark.parametrize("path", ["direct", "fused"])
+def test_direct_big_chunk_path(case, sysname, path, monkeypatch):
+    """Big chunks straight from B (MAGNUS_BIG_PATH=direct, big_direct.cuh, or =fused, fused_big.cuh:
+    no reorder buffer for them; the small chunks' buffer holds small-chunk products only) give the
+    reference's bits."""
+    monkeypatch.setenv("MAGNUS_BIG_PATH", path)
     if case == "hot":
         A, B = _hot_chunk_matrix()
     elif case == "rmat15":
