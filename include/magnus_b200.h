@@ -137,6 +137,12 @@ int magnus_numeric_host(magnus_ctx* ctx, const int64_t* c_row_ptr, uint32_t* c_c
  * reducer), products and distinct columns in the other chunks (sort reducer).  Synchronises. */
 int magnus_heavy_stats(magnus_ctx* ctx, int64_t* out4);
 
+/* Device coarse level (Alg. 4: build_coarse_chunks / coarse_level_batch magnus.py:317-406) of
+ * the last magnus_numeric call: out[0] = Coarse-category rows that went through it, out[1] =
+ * device batches, out[2] = CSC entries (A nonzeros of those rows).  Zeros when no row is Coarse,
+ * or with MAGNUS_COARSE_PATH=fine (the fine-level expand handles them, same bits). */
+int magnus_coarse_level_stats(magnus_ctx* ctx, int64_t* out3);
+
 /* ---- Gustavson baselines (reference gustavson.py:155-268; the ablation without locality generation).
  * Dense: one CTA per row over a full-width accumulator.  scratch (device) must hold at least
  * magnus_gd_scratch_bytes(B->n_cols, 1) bytes; more lets more rows run concurrently (up to 4 per SM).

@@ -76,7 +76,8 @@ EXPORTS = ["magnus_compute_chunk_plan", "magnus_ctx_create", "magnus_ctx_destroy
            "magnus_numeric_host", "magnus_gd_scratch_bytes", "magnus_gd_symbolic", "magnus_gd_numeric",
            "magnus_esc_expand", "magnus_esc_compress", "magnus_mb_histogram", "magnus_mb_reorder_scratch_bytes",
            "magnus_mb_reorder", "magnus_mb_dense", "magnus_mb_stream",
-           "magnus_mb_scan_scratch_bytes", "magnus_mb_scan", "magnus_release_workspace", "magnus_workspace_reserved", "magnus_workspace_bytes", "magnus_set_workspace"]
+           "magnus_mb_scan_scratch_bytes", "magnus_mb_scan", "magnus_release_workspace", "magnus_workspace_reserved", "magnus_workspace_bytes", "magnus_set_workspace",
+           "magnus_coarse_level_stats"]
 KERNEL_NAMES = ["row_stats", "categorize", "sym_warp", "sym_block", "sym_heavy", "scan", "num_warp", "num_block",
                 "num_heavy", "sym_dense", "num_dense", "bin_plan", "bin_expand", "bin_reduce", "bin_big", "dir_index",
                 "dir_plan", "dir_num"]
@@ -113,6 +114,7 @@ def lib():
         L.magnus_profile_enable.argtypes = [C.c_void_p, C.c_int]
         L.magnus_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.magnus_heavy_stats.argtypes = [C.c_void_p, C.c_void_p]
+        L.magnus_coarse_level_stats.argtypes = [C.c_void_p, C.c_void_p]
         L.magnus_compute_chunk_plan.argtypes = [C.POINTER(Sys), C.c_int64, C.c_int, C.c_int, C.POINTER(Plan)]
         L.magnus_gd_scratch_bytes.restype = C.c_size_t
         L.magnus_gd_scratch_bytes.argtypes = [C.c_int64, C.c_int64]
@@ -179,6 +181,12 @@ class Context:
         check(lib().magnus_heavy_stats(self.h, out))
         return {"big_products": int(out[0]), "big_distinct": int(out[1]), "small_products": int(out[2]),
                 "small_distinct": int(out[3])}
+
+    def coarse_level_stats(self) -> dict:
+        """Rows / batches / CSC entries the device coarse level (Alg. 4) handled in the last numeric call."""
+        out = (C.c_int64 * 3)()
+        check(lib().magnus_coarse_level_stats(self.h, out))
+        return {"rows": int(out[0]), "batches": int(out[1]), "csc_entries": int(out[2])}
 
     def profile_read(self) -> dict:
         """{kernel name: (total ms, launches)} since the last read (synchronises)."""

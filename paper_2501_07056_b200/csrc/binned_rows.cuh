@@ -695,7 +695,7 @@ k_bin_expand2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_
               const unsigned long long* __restrict__ nunit, unsigned long long* __restrict__ ticket, int64_t cap_units,
               uint16_t* __restrict__ bcol, double* __restrict__ bval, const int32_t* __restrict__ bslot,
               const uint32_t* __restrict__ bidx, int64_t nwin1, int ilog, uint32_t* __restrict__ gk, int64_t gk_stride,
-              unsigned long long* __restrict__ err) {
+              unsigned long long* __restrict__ err, const int8_t* __restrict__ skip_coarse = nullptr) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);
   double* s_kav = reinterpret_cast<double*>(smem + Exp2Smem::kCnt);
@@ -724,6 +724,8 @@ k_bin_expand2(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int64_
 #endif
     const BinItem it = units[list_slot(u, nu_front, cap_units)];
     const int64_t i = rows[it.h];
+    // rows of the Coarse category are expanded by the coarse level (coarse_rows.cuh)
+    if (skip_coarse != nullptr && skip_coarse[i] == kCatCoarse) continue;
     const int64_t a0 = A.rp(i);
     const int nk = (int)(A.rp(i + 1) - a0);
     const RowBins rb = row_bins(mn[i], mx[i], shift);   // shift <= kSubShift: entries == chunks

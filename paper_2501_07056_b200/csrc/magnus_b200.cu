@@ -18,6 +18,7 @@
 #include "baselines.cuh"
 #include "big_direct.cuh"
 #include "fused_big.cuh"
+#include "coarse_rows.cuh"
 #include "binned_rows.cuh"
 #include "microbench.cuh"
 #include "common.cuh"
@@ -172,7 +173,9 @@ struct magnus_ctx {
   uint32_t* ce = nullptr;     // chunk tables: element prefix / distinct-column prefix
   // direct big-chunk path (big_direct.cuh, MAGNUS_BIG_PATH=direct)
   bool big_direct = false;
-  bool big_fused = false;     // big chunks by k_fu_big (fused_big.cuh, MAGNUS_BIG_PATH=fused)
+  bool big_fused = false;     // big chunks by k_fu_sweep (fused_big.cuh, MAGNUS_BIG_PATH=fused)
+  bool coarse_dev = false;    // Coarse-category heavy rows through the device coarse level (coarse_rows.cuh)
+  int64_t c4_rows = 0, c4_batches = 0, c4_brows = 0;   // last numeric call: coarse rows / batches / CSC entries
   uint32_t* cs = nullptr;     // numeric phase: small-chunk element prefix (big chunks excluded)
   int64_t* hbase_s = nullptr;   // numeric phase: exclusive prefix of the heavy rows' small-chunk products
   std::vector<int64_t> h_small;
@@ -367,6 +370,14 @@ int magnus_profile_read(magnus_ctx* ctx, double* ms, int64_t* launches) {
   return MAGNUS_OK;
 }
 
+int magnus_coarse_level_stats(magnus_ctx* ctx, int64_t* out3) {
+  if (!ctx || !out3) return set_err(MAGNUS_INPUT, "null argument");
+  out3[0] = ctx->c4_rows;
+  out3[1] = ctx->c4_batches;
+  out3[2] = ctx->c4_brows;
+  return MAGNUS_OK;
+}
+
 int magnus_heavy_stats(magnus_ctx* ctx, int64_t* out4) {
   if (!ctx || !out4) return set_err(MAGNUS_INPUT, "null argument");
   for (int q = 0; q < 4; ++q) out4[q] = 0;
@@ -452,6 +463,8 @@ int magnus_ctx_create(magnus_ctx** out) {
                                (int)(mg::bd_warp_smem(mg::kBinMaxShift, mg::kBigD) * mg::kBdW)));
   MG_CUDA(cudaFuncSetAttribute(mg::k_bd_num<mg::kBigDWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)(mg::bd_warp_smem(mg::kBinMaxShift, mg::kBigDWide) * mg::kBdW)));
+  MG_CUDA(cudaFuncSetAttribute(mg::k_c4_fine, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(4 * sizeof(uint32_t) << mg::kC4MaxFineLog)));
   MG_CUDA(cudaFuncSetAttribute(mg::k_fu_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mg::FuSmem::kTotal));
   MG_CUDA(cudaFuncSetAttribute(mg::k_bin_expand2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)mg::Exp2Smem::kTotal));
@@ -890,6 +903,16 @@ int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, cons
     ctx->big_fused = ctx->binned && !ctx->direct && want_fused && ctx->sem.shift_num <= mg::kFuMaxShift;
     ctx->big_direct = ctx->binned && !ctx->direct && ((bp && std::strcmp(bp, "direct") == 0) || ctx->big_fused);
   }
+  {
+    // Coarse-category rows: the coarse level (Alg. 4, coarse_rows.cuh) ahead of the chunk reducers;
+    // MAGNUS_COARSE_PATH=fine sends them through the fine-level expand like every other heavy row
+    const char* cp = std::getenv("MAGNUS_COARSE_PATH");
+    const int64_t csl = ctx->plan_num.shift_coarse - ctx->plan_num.shift_fine;
+    ctx->coarse_dev = ctx->binned && !ctx->direct && !ctx->big_direct && ctx->plan_sym.use_coarse && !force_fine_only &&
+                      !(cp && std::strcmp(cp, "fine") == 0) && ctx->plan_num.n_chunks_coarse <= mg::kC4MaxCoarse &&
+                      csl >= 0 && csl <= mg::kC4MaxFineLog && ctx->plan_num.shift_coarse < 32 &&
+                      ctx->host_stats[mg::kStatNCoarse] > 0;
+  }
   ctx->gshift = mg::bin_shift_of(ctx->sem.shift_num);
   ctx->ncnt = ctx->binned ? (ctx->plan_num.plan_cols >> ctx->gshift) : n_chunks_global;
   const bool chunk_global = ctx->ncnt > mg::kChunkSmem;
@@ -955,6 +978,88 @@ int magnus_categories(magnus_ctx* ctx, int8_t* dst, void* stream) {
   return MAGNUS_OK;
 }
 
+// Coarse level of one batch of heavy rows [h0, h1) (coarse_level_batch magnus.py:379-406): the
+// Coarse-category rows' products, reordered by (row, coarse chunk) from a CSC view of their A
+// rows with every referenced B row read once (build_coarse_chunks magnus.py:317-376), then the
+// fine level per bucket into the reorder buffer (bcol, bval) the chunk reducers read.
+static int coarse_level_batch(magnus_ctx* ctx, int64_t h0, int64_t h1, int64_t batch_base, int64_t batch_elems,
+                              uint16_t* bcol, double* bval) {
+  cudaStream_t s = ctx->stream;
+  const mg::DevCsr& A = ctx->A;
+  const mg::DevCsr& B = ctx->B;
+  const int64_t nB = B.n_rows;
+  mg::C4Geom g;
+  g.sf = (int)ctx->plan_num.shift_fine;
+  g.sc = (int)ctx->plan_num.shift_coarse;
+  g.ncc = (int)ctx->plan_num.n_chunks_coarse;
+  g.h0 = h0;
+  int32_t* list = nullptr;
+  int64_t *apos = nullptr, *colcnt = nullptr, *colptr = nullptr;
+  unsigned long long *colcur = nullptr, *cnt = nullptr;
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&list), (size_t)(h1 - h0 + 1) * 4, s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&apos), (size_t)(h1 - h0 + 1) * 8, s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&colcnt), (size_t)(nB + 1) * 8, s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&colptr), (size_t)(nB + 2) * 8, s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&colcur), (size_t)(nB + 1) * 8, s));
+  MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&cnt), 64, s));
+  MG_CUDA(cudaMemsetAsync(colcnt, 0, (size_t)(nB + 1) * 8, s));
+  MG_CUDA(cudaMemsetAsync(colcur, 0, (size_t)(nB + 1) * 8, s));
+  MG_CUDA(cudaMemsetAsync(cnt, 0, 64, s));
+  const unsigned gw = (unsigned)std::min<int64_t>((h1 - h0 + 7) / 8, (int64_t)ctx->sm_count * 16);
+  ctx->begin(MAGNUS_K_BIN_PLAN);
+  mg::k_c4_rows<<<gw, 256, 0, s>>>(A, ctx->listH, ctx->cat, h0, h1, list, apos, cnt, colcnt);
+  ctx->end();
+  unsigned long long hc[2] = {0, 0};
+  MG_CUDA(cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  const int64_t nlist = (int64_t)hc[0], nnz_a = (int64_t)hc[1];
+  int rc = MAGNUS_OK;
+  if (nlist > 0 && nnz_a > 0) {
+    ctx->c4_rows += nlist;
+    ctx->c4_brows += nnz_a;
+    ++ctx->c4_batches;
+    const int64_t tiles = (nB + mg::kScanTile - 1) / mg::kScanTile;
+    int64_t* tsum = nullptr;
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&tsum), (size_t)(tiles + 1) * 8, s));
+    mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(colcnt, nB, tsum);
+    mg::k_scan_tiles<<<1, 1024, 0, s>>>(tsum, tiles);
+    mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(colcnt, nB, tsum, colptr);
+    ctx->launches += 3;
+    int32_t* csc_h = nullptr;
+    uint32_t *csc_q = nullptr, *koff = nullptr, *ccol = nullptr;
+    double *csc_a = nullptr, *cval = nullptr;
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&csc_h), (size_t)nnz_a * 4, s));
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&csc_q), (size_t)nnz_a * 4, s));
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&csc_a), (size_t)nnz_a * 8, s));
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&koff), (size_t)nnz_a * g.ncc * 4, s));
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&ccol), (size_t)std::max<int64_t>(batch_elems, 1) * 4, s));
+    MG_CUDA(mg_malloc_async(reinterpret_cast<void**>(&cval), (size_t)std::max<int64_t>(batch_elems, 1) * 8, s));
+    const unsigned gl = (unsigned)std::min<int64_t>((nlist + 7) / 8, (int64_t)ctx->sm_count * 16);
+    ctx->begin(MAGNUS_K_BIN_PLAN);
+    mg::k_c4_fill<<<gl, 256, 0, s>>>(A, ctx->listH, list, nlist, apos, h0, colptr, colcur, csc_h, csc_q, csc_a);
+    mg::k_c4_koff<<<gl, 256, 0, s>>>(A, B, ctx->listH, list, nlist, apos, g, ctx->mn, ctx->mx, ctx->choff, ctx->ce,
+                                     ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, koff, ctx->err);
+    ctx->end();
+    ++ctx->launches;
+    ctx->begin(MAGNUS_K_BIN_EXPAND);
+    mg::k_c4_scatter<<<(unsigned)(ctx->sm_count * 4), mg::kC4T, mg::C4Smem::kTotal, s>>>(
+        B, ctx->listH, g, ctx->mn, ctx->mx, ctx->choff, ctx->ce, ctx->hbase, batch_base, colptr, csc_h, csc_q, csc_a, koff,
+        cnt + 2, ccol, cval);
+    const size_t fsm = (size_t)4 * sizeof(uint32_t) << (g.sc - g.sf);
+    mg::k_c4_fine<<<(unsigned)(ctx->sm_count * 8), 128, fsm, s>>>(ctx->listH, list, nlist, g, ctx->mn, ctx->mx, ctx->choff,
+                                                                  ctx->ce, ctx->hbase, batch_base, ccol, cval, cnt + 3, bcol,
+                                                                  bval);
+    ctx->end();
+    ++ctx->launches;
+    if (cudaGetLastError() != cudaSuccess) rc = set_err(MAGNUS_CUDA, "coarse level launch failed");
+    for (void* q : {(void*)tsum, (void*)csc_h, (void*)csc_q, (void*)csc_a, (void*)koff, (void*)ccol, (void*)cval})
+      MG_CUDA(cudaFreeAsync(q, s));
+  }
+  for (void* q : {(void*)list, (void*)apos, (void*)colcnt, (void*)colptr, (void*)colcur, (void*)cnt})
+    MG_CUDA(cudaFreeAsync(q, s));
+  return rc;
+}
+
 // Heavy rows, numeric phase, binned path: batches of rows whose products fit the reorder buffer.
 #ifndef MG_BATCH_FRAC_SERIAL
 #define MG_BATCH_FRAC_SERIAL 0.3
@@ -963,6 +1068,7 @@ static constexpr double kBatchFracSerial = MG_BATCH_FRAC_SERIAL;
 static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, double* c_val) {
   cudaStream_t s = ctx->stream;
   const int64_t nH = ctx->host_stats[mg::kStatNH];
+  ctx->c4_rows = ctx->c4_batches = ctx->c4_brows = 0;
   int64_t max_row = 0, total = 0;
   for (int64_t h = 0; h < nH; ++h) {
     max_row = std::max(max_row, ctx->h_hinter[h]);
@@ -1125,11 +1231,17 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
       plan_batch(b + 1, ctx->aux);
       MG_CUDA(cudaEventRecord(ctx->ev_pl[qn], ctx->aux));
     }
+    if (ctx->coarse_dev) {
+      int rc4 = coarse_level_batch(ctx, cuts[b], cuts[b + 1], hb[b], hb[b + 1] - hb[b], static_cast<uint16_t*>(bcol[q]),
+                                   static_cast<double*>(bval[q]));
+      if (rc4) return rc4;
+    }
     ctx->begin(MAGNUS_K_BIN_EXPAND);
     mg::k_bin_expand2<<<(unsigned)(ctx->sm_count * occ_e2), mg::kE2T, mg::Exp2Smem::kTotal, s>>>(
         ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
         nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]),
-        ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, e2scr, e2_stride, ctx->err);
+        ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, e2scr, e2_stride, ctx->err,
+        ctx->coarse_dev ? ctx->cat : nullptr);
     ctx->end();
     MG_CUDA(cudaEventRecord(ctx->ev_e[q], s));
     // the big-chunk and small-chunk reducers of this batch run on their own streams

@@ -355,3 +355,37 @@ def test_caller_owned_workspace():
     with pytest.raises(InputError):
         plan.numeric(rp, workspace=torch.empty(16, dtype=torch.uint8, device=dev))
     plan.close()
+
+
+COARSE16K = SystemParams(cache_line_bytes=64, l2_bytes=6000)   # m_max 2^16: several coarse chunks for 2^20 columns
+
+
+@pytest.mark.parametrize("case", ["rmat14", "hub", "rmat15", "AB"])
+@pytest.mark.parametrize("sysname", ["coarse", "coarse16k"])
+def test_device_coarse_level(case, sysname, monkeypatch):
+    """Coarse-category rows go through the device coarse level (coarse_rows.cuh: CSC view of the
+    batch's A rows, every referenced B row staged once, row-linked (row, coarse chunk) buckets, fine
+    level per bucket -- reference magnus.py:317-406) and give the reference's bits; so does the
+    fine-level expand (MAGNUS_COARSE_PATH=fine), and several device batches."""
+    from paper_2501_07056_b200 import MagnusPlan
+    if case == "rmat15":
+        A = B = generate.rmat(15, 16, seed=7)
+    else:
+        A, B = CASES[case]()
+    sysp = {"coarse": COARSE, "coarse16k": COARSE16K}[sysname]
+    ref = oracle.spgemm(A, B, sysp)
+    plan = MagnusPlan(A, B, sys=sysp)
+    rp = plan.symbolic()
+    res, _counters = plan.numeric(rp)
+    st = plan.ctx.coarse_level_stats()
+    to_np = lambda t: t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)   # noqa: E731
+    np.testing.assert_array_equal(to_np(res.row_ptr), ref.row_ptr)
+    np.testing.assert_array_equal(to_np(res.col).astype(np.int64) & 0xFFFFFFFF, ref.col.astype(np.int64))
+    np.testing.assert_array_equal(to_np(res.val).view(np.uint64), ref.val.view(np.uint64))
+    if ref.counters["rows_coarse"] > 0 and case != "AB":
+        assert st["rows"] > 0 and st["batches"] >= 1, st   # the coarse level really ran
+    plan.close()
+    monkeypatch.setenv("MAGNUS_BATCH_ELEMS", "300000")   # several heavy-row batches -> several coarse batches
+    assert_same(spgemm_magnus(A, B, sys=sysp), ref)
+    monkeypatch.setenv("MAGNUS_COARSE_PATH", "fine")
+    assert_same(spgemm_magnus(A, B, sys=sysp), ref)
