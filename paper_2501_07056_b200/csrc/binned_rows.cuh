@@ -44,7 +44,7 @@ constexpr int kBinWinT = kBinE / 2;   // window packing quantum
 constexpr int kBinMaxShift = 14;      // chunk width <= 16384 columns (u16 chunk-local columns)
 constexpr int kSubShift = 14;         // table granularity (sub-bin == chunk while shift_num <= 14)
 #ifndef MG_BIN_CUR
-#define MG_BIN_CUR 256
+#define MG_BIN_CUR 128
 #endif
 constexpr int kBinCur = MG_BIN_CUR;   // expand: chunks per unit (cursors / counters in shared memory)
 #ifndef MG_UNIT_MAX

@@ -1,5 +1,6 @@
 """Small products that reach every device kernel class (warp / CTA / dense rows, heavy symbolic,
-expand, big-chunk and small-chunk reducers, the direct big-chunk kernel, fused rows), for
+expand, big-chunk and small-chunk reducers, the direct and fused big-chunk kernels, the coarse
+level, fused rows), for
 compute-sanitizer (memcheck / racecheck / synccheck).  Checks the result against the oracle."""
 import os
 import sys
@@ -14,11 +15,12 @@ from paper_2501_07056_b200 import SystemParams, generate, spgemm_magnus  # noqa:
 
 B200 = SystemParams(cache_line_bytes=128, l2_bytes=232448, memory_budget_bytes=1 << 31)
 FINE4K = SystemParams(cache_line_bytes=64, l2_bytes=4096)
+COARSE = SystemParams(cache_line_bytes=64, l2_bytes=1400)   # Coarse-category rows: the device coarse level
 cases = [("rmat12", generate.rmat(12, 16, seed=3)), ("stencil", generate.stencil27(10))]
 for name, A in cases:
-    for sname, sysp in (("b200", B200), ("fine4k", FINE4K)):
+    for sname, sysp in (("b200", B200), ("fine4k", FINE4K), ("coarse", COARSE)):
         ref = oracle.spgemm(A, A, sysp)
-        for mode in ("", "direct"):
+        for mode in ("", "direct", "fused"):
             if mode:
                 os.environ["MAGNUS_BIG_PATH"] = mode
             else:
