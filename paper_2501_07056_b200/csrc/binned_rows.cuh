@@ -1221,10 +1221,20 @@ constexpr int kBigSV = kBigSE * 8 + 16;    // stage bytes: values (+ alignment s
 #endif
 constexpr int kBigDWide = MG_BIG_DW;            // ranks per pass for chunks with more than kBigD columns
 
+// The wide variant keeps no rank -> column table: its chunks hold more than kBigD distinct
+// columns, so reading the columns back from the bitmap at emission is cheap next to the
+// products, and the 2 bytes per rank buy two more warps per SM.
+#ifndef MG_BIG_WIDE_INV
+#define MG_BIG_WIDE_INV 0
+#endif
+#ifndef MG_BIG_NARROW_INV
+#define MG_BIG_NARROW_INV 1
+#endif
+__host__ __device__ constexpr bool big_has_inv(int D) { return D <= kBigD ? MG_BIG_NARROW_INV != 0 : MG_BIG_WIDE_INV != 0; }
 __host__ __device__ inline size_t bin_big_smem(int shift, int D = kBigD) {
   const size_t width = size_t(1) << shift, words = (width + 31) / 32;
-  return (size_t)D * 8 + (size_t)D * 2 + ((words * 4 + 15) & ~size_t(15)) + ((words * 2 + 15) & ~size_t(15)) +
-         (size_t)kBigNS * (kBigSC + kBigSV) + kBigNS * 8;
+  return (size_t)D * 8 + (big_has_inv(D) ? (size_t)D * 2 : 0) + ((words * 4 + 15) & ~size_t(15)) +
+         ((words * 2 + 15) & ~size_t(15)) + (size_t)kBigNS * (kBigSC + kBigSV) + kBigNS * 8;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -1281,7 +1291,8 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
   unsigned char* stv0 = sp; sp += (size_t)kBigNS * kBigSV;   // 16-byte aligned (kBigD * 8 is)
   unsigned char* stc0 = sp; sp += (size_t)kBigNS * kBigSC;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sp); sp += kBigNS * 8;
-  uint16_t* inv = reinterpret_cast<uint16_t*>(sp); sp += (size_t)D * 2;   // rank - rlo -> column
+  constexpr bool kInv = big_has_inv(D);
+  uint16_t* inv = reinterpret_cast<uint16_t*>(sp); sp += kInv ? (size_t)D * 2 : 0;   // rank - rlo -> column
   uint32_t* bm = reinterpret_cast<uint32_t*>(sp); sp += ((size_t)nwords * 4 + 15) & ~size_t(15);
   uint16_t* pref = reinterpret_cast<uint16_t*>(sp);
   const int lane = threadIdx.x & 31;
@@ -1394,7 +1405,7 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
           const bool valid = r >= rlo && r < rhi;
           const double v = valid ? vs[q] : 0.0;
           const uint32_t key = valid ? r - rlo : 0x10000u + lane;
-          if (valid) inv[key] = cs[q];   // every contributor of a column writes the same value
+          if (kInv && valid) inv[key] = cs[q];   // every contributor of a column writes the same value
           const uint32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
           const uint32_t brk = __ballot_sync(0xffffffffu, valid && lane > 0 && key <= pk);
           if (!brk) {
@@ -1428,9 +1439,27 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
         if (j + kBigNS < nst) issue(j + kBigNS);
       }
       __syncwarp();
-      for (uint32_t r = rlo + lane; r < rhi; r += 32) {
-        __stcs(c_col + out + r, colbase + (uint32_t)inv[r - rlo]);
-        __stcs(c_val + out + r, acc[r - rlo]);
+      if (kInv) {
+        for (uint32_t r = rlo + lane; r < rhi; r += 32) {
+          __stcs(c_col + out + r, colbase + (uint32_t)inv[r - rlo]);
+          __stcs(c_val + out + r, acc[r - rlo]);
+        }
+      } else {
+        // columns from the bitmap: lane per word, the word's ranks start at pref[word]
+        for (int wd = lane; wd < nwords; wd += 32) {
+          uint32_t bits = bm[wd];
+          uint32_t r = pref[wd];
+          if (r >= rhi || r + (uint32_t)__popc(bits) <= rlo) continue;
+          while (bits) {
+            const uint32_t b = (uint32_t)__ffs(bits) - 1u;
+            bits &= bits - 1u;
+            if (r >= rlo && r < rhi) {
+              __stcs(c_col + out + r, colbase + ((uint32_t)wd << 5) + b);
+              __stcs(c_val + out + r, acc[r - rlo]);
+            }
+            ++r;
+          }
+        }
       }
       __syncwarp();
     }
