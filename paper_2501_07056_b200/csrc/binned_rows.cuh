@@ -55,6 +55,12 @@ constexpr uint32_t kBigSplit = 1u << 17;   // big chunks above this many element
 constexpr uint32_t kBigFront = 1u << 14;   // big chunks scheduled first
 constexpr uint32_t kUnitFront = 1u << 15;  // expand units scheduled first
 constexpr int kBigMaxParts = 32;
+#ifndef MG_BIG_WIDE_PARTS
+#define MG_BIG_WIDE_PARTS 1
+#endif
+#ifndef MG_BIG_WIDE_NARROW
+#define MG_BIG_WIDE_NARROW 0
+#endif
 #ifndef MG_BIG_D
 #define MG_BIG_D 1024
 #endif
@@ -220,12 +226,19 @@ __global__ void k_bin_plan(const int32_t* __restrict__ rows, int64_t h0, int64_t
       // big chunks: one item, or column parts of ~kBigSplit elements each (every part
       // streams the whole slice but applies only its own columns)
       if (big) {
-        const int parts = (int)min((uint32_t)kBigMaxParts, (n + kBigSplit - 1) / kBigSplit);
+        int parts = (int)min((uint32_t)kBigMaxParts, (n + kBigSplit - 1) / kBigSplit);
         const bool large = n >= kBigFront;
         // chunks with more distinct columns than one kBigD pass go to the wide-accumulator list
         const uint32_t* dd = cd + choff[h];
         const uint32_t mcols = __ldg(dd + je) - __ldg(dd + js);
-        const bool wide = mcols > (uint32_t)kBigD;
+        bool wide = mcols > (uint32_t)kBigD;
+#if MG_BIG_WIDE_PARTS > 1
+        // tuning: wide chunks as column parts (each part streams the slice and applies its columns)
+        if (wide) {
+          parts = max(parts, MG_BIG_WIDE_PARTS);
+          if (MG_BIG_WIDE_NARROW) wide = false;
+        }
+#endif
         BigItem* bl = wide ? bigs + cap_bigs : bigs;
         unsigned long long* cf = wide ? nwin + 10 : nbig;
         unsigned long long* cb = wide ? nwin + 15 : nbig_back;

@@ -1136,7 +1136,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   const int nbuf = (cuts.size() > 2 && !serial) ? 2 : 1;
   // two plan sets: batch b+1 is planned on a side stream while batch b computes
   const int nitem = cuts.size() > 2 ? 2 : 1;
-  const int64_t max_big = std::max<int64_t>(max_ent, 1) + buf_elems / mg::kBigSplit + 1;
+  const int64_t max_big = std::max<int64_t>(max_ent, 1) * MG_BIG_WIDE_PARTS + buf_elems / mg::kBigSplit + 1;
   void *bcol[2] = {nullptr, nullptr}, *bval[2] = {nullptr, nullptr}, *items[2] = {nullptr, nullptr},
        *cnts[2] = {nullptr, nullptr};
   for (int q = 0; q < nbuf; ++q) {
