@@ -17,7 +17,7 @@
 //                  the bucket sizes are the symbolic pass's chunk-table differences, and the
 //                  row-linked offsets are the reorder-buffer layout itself (bucket (r, c) sits at
 //                  rowbase[r] + ce[r][first fine chunk of c])
-//   k_c4_scatter   one CTA per referenced B row: the row is staged tile by tile in shared memory
+//   k_c4_scatter   one CTA per (referenced B row, 256 CSC entries of its column): the row is staged tile by tile in shared memory
 //                  with bulk async copies (TMA, 16-byte aligned supersets) and reused by every
 //                  CSC entry of its column; products go to the coarse buffer (coarse-chunk-local
 //                  column, a * b) in bucket order = ascending k (Gustavson order per row)
@@ -90,14 +90,19 @@ __global__ void k_c4_fill(DevCsr A, const int32_t* __restrict__ rows, const int3
 }
 
 // Stable position of every A nonzero's segment inside its row's coarse buckets, and the check
-// that the buckets have the sizes the symbolic pass counted.  One warp per coarse row.
-__global__ void k_c4_koff(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int32_t* __restrict__ list,
-                          int64_t nlist, const int64_t* __restrict__ apos, C4Geom g, const int64_t* __restrict__ mn,
-                          const int64_t* __restrict__ mx, const int64_t* __restrict__ choff,
-                          const uint32_t* __restrict__ ce, const int32_t* __restrict__ bslot,
-                          const uint32_t* __restrict__ bidx, int64_t nwin1, int ilog, uint32_t* __restrict__ koff,
-                          unsigned long long* __restrict__ err) {
+// that the buckets have the sizes the symbolic pass counted.  One warp per coarse row: 32 k's at
+// a time, every lane walks its B row once from coarse chunk to coarse chunk (window index for
+// indexed rows, a cursor for the others); run[] (shared memory, one counter per coarse chunk)
+// carries the products of the k's already seen.
+__global__ void __launch_bounds__(256)
+k_c4_koff(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, const int32_t* __restrict__ list, int64_t nlist,
+          const int64_t* __restrict__ apos, C4Geom g, const int64_t* __restrict__ mn, const int64_t* __restrict__ mx,
+          const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce, const int32_t* __restrict__ bslot,
+          const uint32_t* __restrict__ bidx, int64_t nwin1, int ilog, uint32_t* __restrict__ koff,
+          unsigned long long* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
+  uint32_t* run = reinterpret_cast<uint32_t*>(smem) + (size_t)(threadIdx.x >> 5) * g.ncc;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int csl = g.sc - g.sf;
@@ -109,28 +114,52 @@ __global__ void k_c4_koff(DevCsr A, DevCsr B, const int32_t* __restrict__ rows, 
     const RowBins rb = row_bins(mn[i], mx[i], g.sf);
     const uint32_t* e = ce + choff[h];
     const int64_t cc0 = mn[i] >> g.sc, cc1 = mx[i] >> g.sc;
-    for (int64_t cc = cc0; cc <= cc1; ++cc) {
-      const int64_t lo64 = cc << g.sc, hi64 = (cc + 1) << g.sc;
-      const bool hi_all = hi64 >= ((int64_t)1 << 32);
-      uint32_t run = 0;
-      for (int j0 = 0; j0 < nk; j0 += 32) {
-        const int j = j0 + lane;
-        uint32_t len = 0;
-        if (j < nk) {
-          const int64_t k = __ldg(A.col + a0 + j);
-          uint32_t p0 = (uint32_t)B.rp(k), p1 = (uint32_t)B.rp(k + 1);
-          seg_in_window(B, k, p0, p1, (uint32_t)lo64, hi_all ? 0xffffffffu : (uint32_t)hi64, false, hi_all, bslot, bidx, nwin1,
-                        ilog);
-          len = p1 - p0;
+    for (int64_t cc = cc0 + lane; cc <= cc1; cc += 32) run[cc] = 0u;
+    __syncwarp();
+    for (int j0 = 0; j0 < nk; j0 += 32) {
+      const int j = j0 + lane;
+      uint32_t pos = 0, b1 = 0;
+      const uint32_t* ix = nullptr;
+      if (j < nk) {
+        const int64_t k = __ldg(A.col + a0 + j);
+        pos = (uint32_t)B.rp(k);
+        b1 = (uint32_t)B.rp(k + 1);
+        const int32_t sl = bslot != nullptr ? __ldg(bslot + k) : -1;
+        if (sl >= 0) {
+          ix = bidx + (size_t)sl * nwin1;
+          pos = __ldg(ix + min((int64_t)((cc0 << g.sc) >> ilog), nwin1 - 1));
+        } else {
+          pos = lower_bound_col(B.col, pos, b1, (uint32_t)(cc0 << g.sc));
         }
-        const uint32_t inc = warp_incl_scan(len);
-        if (j < nk) koff[(size_t)(ap + j) * g.ncc + cc] = run + inc - len;
-        run += __shfl_sync(0xffffffffu, inc, 31);
       }
-      // bucket size against the symbolic chunk tables
-      const int64_t jl = max((int64_t)0, (cc << csl) - rb.c0), jh = min((int64_t)rb.nchunk, ((cc + 1) << csl) - rb.c0);
-      if (lane == 0 && run != __ldg(e + jh) - __ldg(e + jl)) atomicOr(err, 4ull);
+      for (int64_t cc = cc0; cc <= cc1; ++cc) {
+        const int64_t hi64 = (cc + 1) << g.sc;
+        uint32_t nxt = pos;
+        if (j < nk) {
+          if (hi64 >= ((int64_t)1 << 32)) {
+            nxt = b1;
+          } else if (ix != nullptr) {
+            nxt = __ldg(ix + min(hi64 >> ilog, nwin1 - 1));
+          } else {
+            while (nxt < b1 && __ldg(B.col + nxt) < (uint32_t)hi64) ++nxt;
+          }
+        }
+        const uint32_t len = nxt - pos;
+        pos = nxt;
+        const uint32_t inc = warp_incl_scan(len);
+        const uint32_t base = run[cc];
+        if (j < nk) koff[(size_t)(ap + j) * g.ncc + cc] = base + inc - len;
+        __syncwarp();
+        if (lane == 31) run[cc] = base + inc;
+        __syncwarp();
+      }
     }
+    // bucket sizes against the symbolic chunk tables
+    for (int64_t cc = cc0 + lane; cc <= cc1; cc += 32) {
+      const int64_t jl = max((int64_t)0, (cc << csl) - rb.c0), jh = min((int64_t)rb.nchunk, ((cc + 1) << csl) - rb.c0);
+      if (run[cc] != __ldg(e + jh) - __ldg(e + jl)) atomicOr(err, 4ull);
+    }
+    __syncwarp();
   }
 }
 
@@ -141,24 +170,36 @@ struct C4Smem {
   static constexpr size_t kTotal = kVal + kCol + kBnd + 16;
 };
 
-// Outer-product pass: one CTA per referenced B row (dynamic tickets over k).
+constexpr int kC4Ent = 256;   // CSC entries of one column per work item
+
+// Work items of the outer-product pass: (referenced B row k, chunk of kC4Ent CSC entries of column k).
+__global__ void k_c4_icount(DevCsr B, const int64_t* __restrict__ colptr, int64_t* __restrict__ icnt) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < B.n_rows; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ne = colptr[k + 1] - colptr[k];
+    icnt[k] = (ne > 0 && B.rp(k + 1) > B.rp(k)) ? (ne + kC4Ent - 1) / kC4Ent : 0;
+  }
+}
+
+// Outer-product pass: one CTA per work item (dynamic tickets).  The B row is staged tile by tile
+// in shared memory and reused by the item's CSC entries (one warp per entry at a time).
 __global__ void __launch_bounds__(kC4T)
 k_c4_scatter(DevCsr B, const int32_t* __restrict__ rows, C4Geom g, const int64_t* __restrict__ mn,
              const int64_t* __restrict__ mx, const int64_t* __restrict__ choff, const uint32_t* __restrict__ ce,
              const int64_t* __restrict__ hbase, int64_t batch_base, const int64_t* __restrict__ colptr,
-             const int32_t* __restrict__ csc_h, const uint32_t* __restrict__ csc_q, const double* __restrict__ csc_a,
-             const uint32_t* __restrict__ koff, unsigned long long* __restrict__ ticket, uint32_t* __restrict__ ccol,
-             double* __restrict__ cval) {
+             const int64_t* __restrict__ iptr, const int32_t* __restrict__ csc_h, const uint32_t* __restrict__ csc_q,
+             const double* __restrict__ csc_a, const uint32_t* __restrict__ koff, unsigned long long* __restrict__ ticket,
+             uint32_t* __restrict__ ccol, double* __restrict__ cval) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* s_val = reinterpret_cast<double*>(smem);
   uint32_t* s_col = reinterpret_cast<uint32_t*>(smem + C4Smem::kVal);
   uint32_t* s_bnd = reinterpret_cast<uint32_t*>(smem + C4Smem::kVal + C4Smem::kCol);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C4Smem::kVal + C4Smem::kCol + C4Smem::kBnd);
-  __shared__ long long s_k;
+  __shared__ long long s_k, s_e0;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kC4T / 32;
   const int csl = g.sc - g.sf;
   const uint32_t cmask = g.sc >= 32 ? 0xffffffffu : ((1u << g.sc) - 1u);
+  const int64_t nitems = iptr[B.n_rows];
   if (tid == 0) {
     mbar_init(bar);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -166,96 +207,111 @@ k_c4_scatter(DevCsr B, const int32_t* __restrict__ rows, C4Geom g, const int64_t
   __syncthreads();
   uint32_t fills = 0;
   while (true) {
-    // next referenced B row: tickets are 256-row strips, scanned for non-empty columns
-    if (tid == 0) s_k = (long long)atomicAdd(ticket, 1ull);
-    __syncthreads();
-    const int64_t strip = s_k;
-    __syncthreads();
-    if (strip * 256 >= B.n_rows) break;
-    for (int64_t k = strip * 256; k < min(B.n_rows, (strip + 1) * 256); ++k) {
-      const int64_t e0 = colptr[k], e1 = colptr[k + 1];
-      if (e0 == e1) continue;
-      const uint32_t b0 = (uint32_t)B.rp(k), b1 = (uint32_t)B.rp(k + 1);
-      if (b0 == b1) continue;
-      // coarse chunk boundaries of the row: s_bnd[c] = first position with column >= c << sc
-      for (int c = tid; c <= g.ncc; c += kC4T) {
-        const int64_t key = (int64_t)c << g.sc;
-        s_bnd[c] = key >= ((int64_t)1 << 32) ? b1 : lower_bound_col(B.col, b0, b1, (uint32_t)key);
-      }
-      for (uint32_t t0 = b0; t0 < b1; t0 += kC4Tile) {
-        const uint32_t cnt = min((uint32_t)kC4Tile, b1 - t0);
-        // stage the tile: bulk async copies of 16-byte aligned supersets
-        const uintptr_t ca = reinterpret_cast<uintptr_t>(B.col + t0), va = reinterpret_cast<uintptr_t>(B.val + t0);
-        const uintptr_t ca0 = ca & ~uintptr_t(15), va0 = va & ~uintptr_t(15);
-        const uint32_t cskip = (uint32_t)(ca - ca0) / 4, vskip = (uint32_t)(va - va0) / 8;
-        __syncthreads();   // the previous tile is consumed, the boundaries are written
-        // (the last elements of B are loaded element by element: an aligned superset would read
-        // past the caller's arrays)
-        const bool bulk = (int64_t)t0 + cnt + 4 <= B.nnz;
-        if (bulk) {
-          if (tid == 0) {
-            const uint32_t cb = (uint32_t)(((ca + (size_t)cnt * 4 - ca0) + 15) & ~uintptr_t(15));
-            const uint32_t vb = (uint32_t)(((va + (size_t)cnt * 8 - va0) + 15) & ~uintptr_t(15));
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            bulk_load2(bar, s_col, reinterpret_cast<const void*>(ca0), cb, s_val, reinterpret_cast<const void*>(va0), vb);
-          }
-          mbar_wait(bar, fills & 1u);
-          ++fills;
-        } else {
-          for (uint32_t t = tid; t < cnt; t += kC4T) {
-            s_col[cskip + t] = __ldg(B.col + t0 + t);
-            s_val[vskip + t] = __ldg(B.val + t0 + t);
-          }
-          __syncthreads();
+    if (tid == 0) {
+      const long long t = (long long)atomicAdd(ticket, 1ull);
+      long long k = -1, e0 = 0;
+      if (t < nitems) {
+        int64_t lo = 0, hi = B.n_rows;   // last k with iptr[k] <= t
+        while (hi - lo > 1) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (iptr[mid] <= t) lo = mid; else hi = mid;
         }
-        const uint32_t* tc = s_col + cskip;
-        const double* tv = s_val + vskip;
-        // every CSC entry of the column reuses the staged tile
-        for (int64_t en = e0 + wid; en < e1; en += NW) {
-          const int32_t h = __ldg(csc_h + en);
-          const uint32_t q = __ldg(csc_q + en);
-          const double a = __ldg(csc_a + en);
-          const int64_t i = rows[h];
-          const int64_t c0 = mn[i] >> g.sf;
-          const int64_t rowbase = hbase[h] - batch_base;
-          const uint32_t* e = ce + choff[h];
-          const uint32_t* ko = koff + (size_t)q * g.ncc;
-          for (uint32_t t = lane; t < cnt; t += 32) {
-            const uint32_t col = tc[t];
-            const uint32_t cc = g.sc >= 32 ? 0u : col >> g.sc;
-            const int64_t jl = max((int64_t)0, ((int64_t)cc << csl) - c0);
-            const int64_t dst = rowbase + __ldg(e + jl) + __ldg(ko + cc) + ((t0 + t) - s_bnd[cc]);
-            ccol[dst] = col & cmask;
-            cval[dst] = __dmul_rn(a, tv[t]);
-          }
+        k = lo;
+        e0 = colptr[k] + (t - iptr[k]) * kC4Ent;
+      }
+      s_k = k;
+      s_e0 = e0;
+    }
+    __syncthreads();
+    const int64_t k = s_k, e0 = s_e0;
+    __syncthreads();
+    if (k < 0) break;
+    const int64_t e1 = min(colptr[k + 1], e0 + kC4Ent);
+    const uint32_t b0 = (uint32_t)B.rp(k), b1 = (uint32_t)B.rp(k + 1);
+    for (uint32_t t0 = b0; t0 < b1; t0 += kC4Tile) {
+      const uint32_t cnt = min((uint32_t)kC4Tile, b1 - t0);
+      // coarse chunks the tile touches: s_bnd[c - c_lo] = first position of the row with column >= c << sc
+      const uint32_t c_lo = g.sc >= 32 ? 0u : __ldg(B.col + t0) >> g.sc;
+      const uint32_t c_hi = g.sc >= 32 ? 0u : __ldg(B.col + t0 + cnt - 1) >> g.sc;
+      // stage the tile: bulk async copies of 16-byte aligned supersets
+      const uintptr_t ca = reinterpret_cast<uintptr_t>(B.col + t0), va = reinterpret_cast<uintptr_t>(B.val + t0);
+      const uintptr_t ca0 = ca & ~uintptr_t(15), va0 = va & ~uintptr_t(15);
+      const uint32_t cskip = (uint32_t)(ca - ca0) / 4, vskip = (uint32_t)(va - va0) / 8;
+      __syncthreads();   // the previous tile is consumed
+      for (uint32_t c = c_lo + tid; c <= c_hi; c += kC4T)
+        s_bnd[c - c_lo] = lower_bound_col(B.col, b0, b1, c << g.sc);
+      // (the last elements of B are loaded element by element: an aligned superset would read
+      // past the caller's arrays)
+      const bool bulk = (int64_t)t0 + cnt + 4 <= B.nnz;
+      if (bulk) {
+        if (tid == 0) {
+          const uint32_t cb = (uint32_t)(((ca + (size_t)cnt * 4 - ca0) + 15) & ~uintptr_t(15));
+          const uint32_t vb = (uint32_t)(((va + (size_t)cnt * 8 - va0) + 15) & ~uintptr_t(15));
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          bulk_load2(bar, s_col, reinterpret_cast<const void*>(ca0), cb, s_val, reinterpret_cast<const void*>(va0), vb);
+        }
+        mbar_wait(bar, fills & 1u);
+        ++fills;
+      } else {
+        for (uint32_t t = tid; t < cnt; t += kC4T) {
+          s_col[cskip + t] = __ldg(B.col + t0 + t);
+          s_val[vskip + t] = __ldg(B.val + t0 + t);
         }
       }
-      __syncthreads();   // s_bnd is rewritten for the next row
+      __syncthreads();   // boundaries written (and the element-wise tile)
+      const uint32_t* tc = s_col + cskip;
+      const double* tv = s_val + vskip;
+      // every CSC entry of the item reuses the staged tile
+      for (int64_t en = e0 + wid; en < e1; en += NW) {
+        const int32_t h = __ldg(csc_h + en);
+        const uint32_t q = __ldg(csc_q + en);
+        const double a = __ldg(csc_a + en);
+        const int64_t i = rows[h];
+        const int64_t c0 = mn[i] >> g.sf;
+        const int64_t rowbase = hbase[h] - batch_base;
+        const uint32_t* e = ce + choff[h];
+        const uint32_t* ko = koff + (size_t)q * g.ncc;
+        for (uint32_t t = lane; t < cnt; t += 32) {
+          const uint32_t col = tc[t];
+          const uint32_t cc = g.sc >= 32 ? 0u : col >> g.sc;
+          const int64_t jl = max((int64_t)0, ((int64_t)cc << csl) - c0);
+          const int64_t dst = rowbase + __ldg(e + jl) + __ldg(ko + cc) + ((t0 + t) - s_bnd[cc - c_lo]);
+          ccol[dst] = col & cmask;
+          cval[dst] = __dmul_rn(a, tv[t]);
+        }
+      }
     }
   }
 }
 
-// Fine level of one (row, coarse chunk) bucket: one warp reads the bucket in order and appends
-// every element to its fine chunk's slice (stable).  Buckets by dynamic tickets.
-__global__ void __launch_bounds__(128)
+// Fine level of one (row, coarse chunk) bucket: one CTA reads the bucket in order -- four
+// contiguous warp ranges -- and appends every element to its fine chunk's slice.  Pass 1 counts
+// each warp's elements per fine chunk, a prefix over the warps gives every warp its first slot
+// in every slice, pass 2 scatters (stable: warp ranges are in bucket order, lanes of one wave
+// are ranked in lane order).  Buckets by dynamic tickets.
+constexpr int kC4FT = 128;
+__global__ void __launch_bounds__(kC4FT)
 k_c4_fine(const int32_t* __restrict__ rows, const int32_t* __restrict__ list, int64_t nlist, C4Geom g,
           const int64_t* __restrict__ mn, const int64_t* __restrict__ mx, const int64_t* __restrict__ choff,
           const uint32_t* __restrict__ ce, const int64_t* __restrict__ hbase, int64_t batch_base,
           const uint32_t* __restrict__ ccol, const double* __restrict__ cval, unsigned long long* __restrict__ ticket,
           uint16_t* __restrict__ bcol, double* __restrict__ bval) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int NW = kC4FT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int csl = g.sc - g.sf;
   const int nf = 1 << csl;
-  uint32_t* cur = reinterpret_cast<uint32_t*>(smem) + (size_t)wid * nf;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem);   // [NW][nf]
+  uint32_t* cur = cnt + (size_t)wid * nf;
+  __shared__ long long s_t;
   const uint32_t fmask = (1u << g.sf) - 1u, lt = lanemask_lt();
   const int64_t nb = nlist * g.ncc;   // (row, coarse chunk) pairs; empty ones cost one ticket
-  unsigned long long tn = 0;
-  if (lane == 0) tn = atomicAdd(ticket, 1ull);
   while (true) {
-    const int64_t t = (int64_t)__shfl_sync(0xffffffffu, tn, 0);
+    if (tid == 0) s_t = (long long)atomicAdd(ticket, 1ull);
+    __syncthreads();
+    const int64_t t = s_t;
+    __syncthreads();
     if (t >= nb) break;
-    if (lane == 0) tn = atomicAdd(ticket, 1ull);
     const int32_t h = list[t / g.ncc];
     const int64_t cc = t % g.ncc;
     const int64_t i = rows[h];
@@ -266,13 +322,27 @@ k_c4_fine(const int32_t* __restrict__ rows, const int32_t* __restrict__ list, in
     const uint32_t s0 = __ldg(e + jl), s1 = __ldg(e + jh);
     if (s0 == s1) continue;
     const int64_t rowbase = hbase[h] - batch_base;
-    // row-relative fine chunk of coarse-local fine chunk f: (cc << csl) + f - c0
-    const int64_t jrel = (cc << csl) - rb.c0;
-    for (int f = lane; f < nf; f += 32) cur[f] = 0u;
-    __syncwarp();
-    for (uint32_t q0 = s0; q0 < s1; q0 += 32) {
+    const int64_t jrel = (cc << csl) - rb.c0;   // row-relative fine chunk of the coarse chunk's first fine chunk
+    const uint32_t n = s1 - s0;
+    const uint32_t L = ((n + NW - 1) / NW + 31) & ~31u;
+    const uint32_t q_beg = s0 + min(n, (uint32_t)wid * L), q_end = s0 + min(n, (uint32_t)(wid + 1) * L);
+    for (int f = tid; f < NW * nf; f += kC4FT) cnt[f] = 0u;
+    __syncthreads();
+    for (uint32_t q = q_beg + lane; q < q_end; q += 32) atomicAdd(&cur[__ldg(ccol + rowbase + q) >> g.sf], 1u);
+    __syncthreads();
+    for (int f = tid; f < nf; f += kC4FT) {
+      uint32_t run = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        const uint32_t v = cnt[(size_t)w * nf + f];
+        cnt[(size_t)w * nf + f] = run;
+        run += v;
+      }
+    }
+    __syncthreads();
+    for (uint32_t q0 = q_beg; q0 < q_end; q0 += 32) {
       const uint32_t q = q0 + lane;
-      const bool valid = q < s1;
+      const bool valid = q < q_end;
       const uint32_t lc = valid ? __ldg(ccol + rowbase + q) : 0u;
       const double v = valid ? __ldg(cval + rowbase + q) : 0.0;
       const uint32_t f = valid ? lc >> g.sf : 0x40000000u + lane;

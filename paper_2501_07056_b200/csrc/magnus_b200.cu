@@ -1037,14 +1037,22 @@ static int coarse_level_batch(magnus_ctx* ctx, int64_t h0, int64_t h1, int64_t b
     const unsigned gl = (unsigned)std::min<int64_t>((nlist + 7) / 8, (int64_t)ctx->sm_count * 16);
     ctx->begin(MAGNUS_K_BIN_PLAN);
     mg::k_c4_fill<<<gl, 256, 0, s>>>(A, ctx->listH, list, nlist, apos, h0, colptr, colcur, csc_h, csc_q, csc_a);
-    mg::k_c4_koff<<<gl, 256, 0, s>>>(A, B, ctx->listH, list, nlist, apos, g, ctx->mn, ctx->mx, ctx->choff, ctx->ce,
+    mg::k_c4_koff<<<gl, 256, (size_t)8 * g.ncc * 4, s>>>(A, B, ctx->listH, list, nlist, apos, g, ctx->mn, ctx->mx, ctx->choff, ctx->ce,
                                      ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, koff, ctx->err);
     ctx->end();
     ++ctx->launches;
+    // work items of the outer-product pass: (B row, 256 CSC entries); item pointers reuse colcnt / colcur
+    int64_t* icnt = colcnt;
+    int64_t* iptr = reinterpret_cast<int64_t*>(colcur);
+    mg::k_c4_icount<<<(unsigned)std::min<int64_t>((nB + 255) / 256, (int64_t)ctx->sm_count * 16), 256, 0, s>>>(B, colptr, icnt);
+    mg::k_scan_reduce<<<(unsigned)tiles, mg::kScanT, 0, s>>>(icnt, nB, tsum);
+    mg::k_scan_tiles<<<1, 1024, 0, s>>>(tsum, tiles);
+    mg::k_scan_apply<<<(unsigned)tiles, mg::kScanT, 0, s>>>(icnt, nB, tsum, iptr);
+    ctx->launches += 4;
     ctx->begin(MAGNUS_K_BIN_EXPAND);
     mg::k_c4_scatter<<<(unsigned)(ctx->sm_count * 4), mg::kC4T, mg::C4Smem::kTotal, s>>>(
-        B, ctx->listH, g, ctx->mn, ctx->mx, ctx->choff, ctx->ce, ctx->hbase, batch_base, colptr, csc_h, csc_q, csc_a, koff,
-        cnt + 2, ccol, cval);
+        B, ctx->listH, g, ctx->mn, ctx->mx, ctx->choff, ctx->ce, ctx->hbase, batch_base, colptr, iptr, csc_h, csc_q, csc_a,
+        koff, cnt + 2, ccol, cval);
     const size_t fsm = (size_t)4 * sizeof(uint32_t) << (g.sc - g.sf);
     mg::k_c4_fine<<<(unsigned)(ctx->sm_count * 8), 128, fsm, s>>>(ctx->listH, list, nlist, g, ctx->mn, ctx->mx, ctx->choff,
                                                                   ctx->ce, ctx->hbase, batch_base, ccol, cval, cnt + 3, bcol,
