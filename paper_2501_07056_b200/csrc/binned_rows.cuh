@@ -1458,7 +1458,9 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
           __stcs(c_val + out + r, acc[r - rlo]);
         }
       } else {
-        // columns from the bitmap: lane per word, the word's ranks start at pref[word]
+        // values in rank order (coalesced); columns from the bitmap: lane per word, the word's
+        // ranks start at pref[word]
+        for (uint32_t r = rlo + lane; r < rhi; r += 32) __stcs(c_val + out + r, acc[r - rlo]);
         for (int wd = lane; wd < nwords; wd += 32) {
           uint32_t bits = bm[wd];
           uint32_t r = pref[wd];
@@ -1466,10 +1468,7 @@ k_bin_big(Sem sem, const BigItem* __restrict__ bigs, const unsigned long long* _
           while (bits) {
             const uint32_t b = (uint32_t)__ffs(bits) - 1u;
             bits &= bits - 1u;
-            if (r >= rlo && r < rhi) {
-              __stcs(c_col + out + r, colbase + ((uint32_t)wd << 5) + b);
-              __stcs(c_val + out + r, acc[r - rlo]);
-            }
+            if (r >= rlo && r < rhi) __stcs(c_col + out + r, colbase + ((uint32_t)wd << 5) + b);
             ++r;
           }
         }

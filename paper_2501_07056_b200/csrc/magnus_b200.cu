@@ -16,6 +16,8 @@
 
 #include "../../include/magnus_b200.h"
 #include "baselines.cuh"
+#include <nvtx3/nvToolsExt.h>
+
 #include "big_direct.cuh"
 #include "fused_big.cuh"
 #include "coarse_rows.cuh"
@@ -47,6 +49,15 @@ int set_err(int code, const std::string& msg) {
 #else
 #define DIR_SYNC(what) do { } while (0)
 #endif
+
+// NVTX ranges around the phases and the heavy-row batches (visible in Nsight Systems / Compute;
+// nvtx3 is header-only and a no-op without an attached tool).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // MAGNUS_TRACE=1: host timestamps of magnus_setup's steps on stderr (synchronising)
 static void trace_point(cudaStream_t s, const char* what) {
@@ -688,6 +699,7 @@ static int validate_inputs(magnus_ctx* ctx, const magnus_csr& A, const magnus_cs
 int magnus_setup(magnus_ctx* ctx, const magnus_csr* A, const magnus_csr* B, const magnus_sys* sys,
                  const magnus_thresholds* th, int force_fine_only, void* stream) {
   if (!ctx || !A || !B || !sys || !th) return set_err(MAGNUS_INPUT, "null argument");
+  NvtxRange nvtx_range("magnus_setup");
   if (A->n_cols != B->n_rows)   // _check_dims gustavson.py:39-41
     return set_err(MAGNUS_INPUT, "dimension mismatch: A is " + std::to_string(A->n_rows) + "x" + std::to_string(A->n_cols) +
                                      ", B is " + std::to_string(B->n_rows) + "x" + std::to_string(B->n_cols));
@@ -1217,6 +1229,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
   };
   plan_batch(0, s);
   for (size_t b = 0; b + 1 < cuts.size(); ++b) {
+    NvtxRange nvtx_batch("magnus heavy-row batch");
     const int q = (int)(b % nbuf);
     const int qi = (int)(b % nitem);
     mg::BinItem* wins = static_cast<mg::BinItem*>(items[qi]);
@@ -1736,6 +1749,7 @@ static int launch_light(magnus_ctx* ctx, bool numeric, const int64_t* c_rp, uint
 
 int magnus_symbolic(magnus_ctx* ctx, int64_t* c_row_ptr, int64_t* nnz_out, void* stream) {
   if (!ctx || !ctx->ready) return set_err(MAGNUS_CONTRACT, "magnus_setup has not run");
+  NvtxRange nvtx_range("magnus_symbolic");
   ctx->stream = (cudaStream_t)stream;
   cudaStream_t s = ctx->stream;
   const int64_t n = ctx->A.n_rows;
@@ -1769,6 +1783,7 @@ int magnus_numeric(magnus_ctx* ctx, const int64_t* c_row_ptr, uint32_t* c_col, d
                    void* stream) {
   if (!ctx || !ctx->ready) return set_err(MAGNUS_CONTRACT, "magnus_setup has not run");
   if (!ctx->have_symbolic) return set_err(MAGNUS_CONTRACT, "row_ptr does not come from a symbolic pass of (A, B)");
+  NvtxRange nvtx_range("magnus_numeric");
   ctx->stream = (cudaStream_t)stream;
   cudaStream_t s = ctx->stream;
   if (ctx->A.n_rows > 0) {
