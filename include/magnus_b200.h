@@ -184,6 +184,13 @@ int magnus_mb_dense(const uint32_t* col, const double* val, const int64_t* offse
 /* exclusive prefix sum: out[0..n] (out[n] = total) of int64 in[0..n); scratch of magnus_mb_scan_scratch_bytes(n). */
 size_t magnus_mb_scan_scratch_bytes(int64_t n);
 int magnus_mb_scan(const int64_t* in, int64_t n, int64_t* out, void* scratch, void* stream);
+/* stable sort of (key, position) pairs (LSD radix sort, 8-bit digits; one pass per byte of key_mask with a set bit --
+ * key_mask covers every bit that can differ between keys): keys_out = the keys ascending, perm_out[j] = position in
+ * `keys` of the j-th smallest (np.argsort(kind="stable"), reference bench.py:160-180 / accumulators.py:113-129).
+ * scratch (device) of magnus_sort_pairs_scratch_bytes(n) bytes; keys_out / perm_out must not alias keys. */
+size_t magnus_sort_pairs_scratch_bytes(int64_t n);
+int magnus_sort_pairs(const uint64_t* keys, int64_t n, uint64_t key_mask, uint64_t* keys_out, int64_t* perm_out,
+                      void* scratch, void* stream);
 /* contiguous copy (the streaming baseline): bytes (multiple of 16, 16-byte aligned). */
 int magnus_mb_stream(const void* src, void* dst, int64_t bytes, void* stream);
 

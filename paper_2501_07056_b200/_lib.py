@@ -77,7 +77,7 @@ EXPORTS = ["magnus_compute_chunk_plan", "magnus_ctx_create", "magnus_ctx_destroy
            "magnus_esc_expand", "magnus_esc_compress", "magnus_mb_histogram", "magnus_mb_reorder_scratch_bytes",
            "magnus_mb_reorder", "magnus_mb_dense", "magnus_mb_stream",
            "magnus_mb_scan_scratch_bytes", "magnus_mb_scan", "magnus_release_workspace", "magnus_workspace_reserved", "magnus_workspace_bytes", "magnus_set_workspace",
-           "magnus_coarse_level_stats"]
+           "magnus_coarse_level_stats", "magnus_sort_pairs_scratch_bytes", "magnus_sort_pairs"]
 KERNEL_NAMES = ["row_stats", "categorize", "sym_warp", "sym_block", "sym_heavy", "scan", "num_warp", "num_block",
                 "num_heavy", "sym_dense", "num_dense", "bin_plan", "bin_expand", "bin_reduce", "bin_big", "dir_index",
                 "dir_plan", "dir_num"]
@@ -115,6 +115,9 @@ def lib():
         L.magnus_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.magnus_heavy_stats.argtypes = [C.c_void_p, C.c_void_p]
         L.magnus_coarse_level_stats.argtypes = [C.c_void_p, C.c_void_p]
+        L.magnus_sort_pairs_scratch_bytes.restype = C.c_size_t
+        L.magnus_sort_pairs_scratch_bytes.argtypes = [C.c_int64]
+        L.magnus_sort_pairs.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.magnus_compute_chunk_plan.argtypes = [C.POINTER(Sys), C.c_int64, C.c_int, C.c_int, C.POINTER(Plan)]
         L.magnus_gd_scratch_bytes.restype = C.c_size_t
         L.magnus_gd_scratch_bytes.argtypes = [C.c_int64, C.c_int64]
@@ -195,6 +198,24 @@ class Context:
         cnt = (C.c_int64 * n)()
         check(lib().magnus_profile_read(self.h, ms, cnt))
         return {KERNEL_NAMES[k]: (float(ms[k]), int(cnt[k])) for k in range(n)}
+
+
+def sort_pairs(keys, key_bits: int = 64, key_mask: int = None):
+    """Stable ascending sort of non-negative int64 CUDA keys with the library's own LSD radix sort
+    (csrc/radix_sort.cuh): returns (sorted keys, permutation), like torch.sort(keys, stable=True).  The keys may
+    differ only in their low `key_bits` bits, or in the bits of `key_mask` (bytes without a set bit cost no pass)."""
+    import torch
+
+    n = int(keys.numel())
+    out = torch.empty_like(keys)
+    perm = torch.empty(n, dtype=torch.int64, device=keys.device)
+    if n:
+        scratch = torch.empty(int(lib().magnus_sort_pairs_scratch_bytes(n)), dtype=torch.uint8, device=keys.device)
+        mask = int(key_mask) if key_mask is not None else (1 << min(int(key_bits), 64)) - 1
+        check(lib().magnus_sort_pairs(C.c_void_p(keys.data_ptr()), n, C.c_uint64(mask & 0xFFFFFFFFFFFFFFFF), C.c_void_p(out.data_ptr()),
+                                      C.c_void_p(perm.data_ptr()), C.c_void_p(scratch.data_ptr()),
+                                      C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out, perm
 
 
 def release_workspace() -> None:

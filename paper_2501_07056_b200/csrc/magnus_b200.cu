@@ -21,6 +21,7 @@
 #include "big_direct.cuh"
 #include "fused_big.cuh"
 #include "coarse_rows.cuh"
+#include "radix_sort.cuh"
 #include "binned_rows.cuh"
 #include "microbench.cuh"
 #include "common.cuh"
@@ -2038,6 +2039,51 @@ int magnus_mb_dense(const uint32_t* col, const double* val, const int64_t* offse
   MG_CUDA(cudaFuncSetAttribute(mg::k_mb_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh));
   mg::k_mb_dense<<<(unsigned)n_chunks, 32, sh, (cudaStream_t)stream>>>(col, val, offsets, n_chunks, chunk_len, out_col,
                                                                        out_val, distinct);
+  MG_CUDA(cudaGetLastError());
+  return MAGNUS_OK;
+}
+
+// Stable LSD radix sort of (key, position): the sort stage of the sort-accumulator microbenchmark.
+size_t magnus_sort_pairs_scratch_bytes(int64_t n) {
+  const int64_t ntiles = (std::max<int64_t>(n, 1) + mg::kRsTile - 1) / mg::kRsTile;
+  const int64_t nh = 256 * ntiles;
+  return (size_t)std::max<int64_t>(n, 1) * 16 + (size_t)(2 * nh + 2) * 8 + (size_t)((nh + mg::kScanTile - 1) / mg::kScanTile + 2) * 8 + 64;
+}
+
+int magnus_sort_pairs(const uint64_t* keys, int64_t n, uint64_t key_mask, uint64_t* keys_out, int64_t* perm_out,
+                      void* scratch, void* stream) {
+  if (n < 0 || (n && (!keys || !keys_out || !perm_out || !scratch))) return set_err(MAGNUS_INPUT, "sort_pairs: bad argument");
+  if (!n) return MAGNUS_OK;
+  if (!key_mask) key_mask = 0xffull;   // nothing to order by: one pass copies the keys and writes the identity
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t ntiles = (n + mg::kRsTile - 1) / mg::kRsTile, nh = 256 * ntiles;
+  unsigned char* sp = static_cast<unsigned char*>(scratch);
+  uint64_t* tk = reinterpret_cast<uint64_t*>(sp); sp += (size_t)n * 8;
+  int64_t* tp = reinterpret_cast<int64_t*>(sp); sp += (size_t)n * 8;
+  int64_t* hist = reinterpret_cast<int64_t*>(sp); sp += (size_t)nh * 8;
+  int64_t* base = reinterpret_cast<int64_t*>(sp); sp += (size_t)(nh + 2) * 8;
+  int64_t* tsum = reinterpret_cast<int64_t*>(sp);
+  // one pass per key byte that has a significant bit
+  int shifts[8], passes = 0;
+  for (int b = 0; b < 8; ++b)
+    if ((key_mask >> (8 * b)) & 0xffull) shifts[passes++] = 8 * b;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)sm_count() * 16);
+  const int64_t stiles = (nh + mg::kScanTile - 1) / mg::kScanTile;
+  const uint64_t* src_k = keys;
+  const int64_t* src_p = nullptr;
+  for (int p = 0; p < passes; ++p) {
+    // the last pass writes the caller's arrays: out on passes with the parity of passes - 1
+    const bool to_out = ((passes - 1 - p) & 1) == 0;
+    uint64_t* dk = to_out ? keys_out : tk;
+    int64_t* dp = to_out ? perm_out : tp;
+    mg::k_rs_hist<<<grid, mg::kRsT, 0, s>>>(src_k, n, shifts[p], ntiles, hist);
+    mg::k_scan_reduce<<<(unsigned)stiles, mg::kScanT, 0, s>>>(hist, nh, tsum);
+    mg::k_scan_tiles<<<1, 1024, 0, s>>>(tsum, stiles);
+    mg::k_scan_apply<<<(unsigned)stiles, mg::kScanT, 0, s>>>(hist, nh, tsum, base);
+    mg::k_rs_scatter<<<grid, mg::kRsT, 0, s>>>(src_k, src_p, n, shifts[p], ntiles, base, dk, dp);
+    src_k = dk;
+    src_p = dp;
+  }
   MG_CUDA(cudaGetLastError());
   return MAGNUS_OK;
 }

@@ -15,14 +15,15 @@ type and counters as the reference:
 Values follow the reference bit for bit: dense = sequential from +0.0 in
 Gustavson order (DenseAccumulator), ESC = x0 + pairwise(rest)
 (sort_accumulate).  Kernels: csrc/baselines.cuh behind the C-ABI
-`magnus_gd_*` / `magnus_esc_*`; the ESC sort step is torch.sort (CUB radix
-sort, stable) -- a library sort is what an ESC baseline uses.  There is no
-CPU fallback.
+`magnus_gd_*` / `magnus_esc_*`; the ESC sort step is the library's own stable
+LSD radix sort (csrc/radix_sort.cuh; MAGNUS_ESC_SORT=cub selects torch.sort).
+There is no CPU fallback.
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import os as _os
 import time
 
 import numpy as np
@@ -161,7 +162,13 @@ def _esc_numeric(P: _Pair, rp, batch_products: int = ESC_BATCH_PRODUCTS):
             vals = torch.empty(m, dtype=torch.float64, device=P.device)
             _lib.check(L.magnus_esc_expand(C.byref(P.a), C.byref(P.b), r0, r1, C.c_void_p(off.data_ptr()),
                                            C.c_void_p(keys.data_ptr()), C.c_void_p(vals.data_ptr()), P.sp()))
-            skeys, perm = torch.sort(keys, stable=True)
+            # stable sort by (row, column): the library's own LSD radix sort over the key bytes that can differ
+            # (MAGNUS_ESC_SORT=cub: torch.sort)
+            if _os.environ.get("MAGNUS_ESC_SORT") == "cub":
+                skeys, perm = torch.sort(keys, stable=True)
+            else:
+                mask = ((1 << max(1, int(P.B.n_cols - 1).bit_length())) - 1) | (((1 << max(1, int(r1 - r0 - 1).bit_length())) - 1) << 32)
+                skeys, perm = _lib.sort_pairs(keys, key_mask=mask)
             del keys
             run = torch.empty(m + 1, dtype=torch.int64, device=P.device)
             runs = C.c_int64(0)

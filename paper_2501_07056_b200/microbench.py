@@ -17,7 +17,8 @@ permutation with intra-chunk stability, distinct counts agree between the two
 accumulators and with the stream, value sums are conserved), so timing never
 bypasses verification.  Times are CUDA-event times on the launching stream.
 Differences from the reference: the stream lives in HBM (u32 indices); the
-sort accumulator's sort step is torch.sort (CUB); chunk counts are bounded by
+sort accumulator's sort step is the library's own stable LSD radix sort
+(csrc/radix_sort.cuh, `magnus_sort_pairs`); chunk counts are bounded by
 shared memory (reorder <= 4096 chunks, dense chunk length <= 16384).
 """
 
@@ -176,7 +177,7 @@ def microbench_building_blocks(spec: StreamSpec, n_chunks: int, reps: int = 1, r
 
         def sort_accum():
             keys = col_out.to(torch.int64) + torch.repeat_interleave(torch.arange(n_chunks, device=dev), counts) * chunk_len
-            sk, perm = torch.sort(keys, stable=True)
+            sk, perm = _lib.sort_pairs(keys, max(1, int(span - 1).bit_length()))
             runs = C.c_int64(0)
             _lib.check(L.magnus_esc_compress(ptr(sk), ptr(perm), ptr(val_out), n, 0, ptr(s_col), ptr(s_val), ptr(run),
                                              C.byref(runs), sp))

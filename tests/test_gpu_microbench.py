@@ -76,3 +76,19 @@ def test_input_errors():
         microbench.microbench_building_blocks(microbench.StreamSpec(100, 64), 128)
     with pytest.raises(InputError):
         microbench.StreamSpec(10, 0)
+
+
+@pytest.mark.parametrize("n,bits", [(0, 8), (1, 1), (1000, 10), (4097, 20), ((1 << 20) + 3, 20), (300000, 52)])
+def test_sort_pairs_matches_stable_sort(n, bits):
+    """magnus_sort_pairs (hand-written LSD radix sort, csrc/radix_sort.cuh) == a stable sort of the keys: sorted keys and
+    the permutation (ties keep their order), for few and many distinct keys."""
+    from paper_2501_07056_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(n + bits)
+    hi = min(1 << bits, 1 << 62)
+    keys = torch.randint(0, hi, (n,), dtype=torch.int64, device="cuda", generator=g)
+    if n > 10:
+        keys[::7] = keys[3]   # many ties
+    sk, perm = _lib.sort_pairs(keys, bits)
+    rk, rperm = torch.sort(keys, stable=True)
+    assert torch.equal(sk, rk)
+    assert torch.equal(perm, rperm)
