@@ -996,7 +996,8 @@ int magnus_categories(magnus_ctx* ctx, int8_t* dst, void* stream) {
 // rows with every referenced B row read once (build_coarse_chunks magnus.py:317-376), then the
 // fine level per bucket into the reorder buffer (bcol, bval) the chunk reducers read.
 static int coarse_level_batch(magnus_ctx* ctx, int64_t h0, int64_t h1, int64_t batch_base, int64_t batch_elems,
-                              uint16_t* bcol, double* bval) {
+                              uint16_t* bcol, double* bval, bool* handled) {
+  *handled = false;
   cudaStream_t s = ctx->stream;
   const mg::DevCsr& A = ctx->A;
   const mg::DevCsr& B = ctx->B;
@@ -1027,7 +1028,11 @@ static int coarse_level_batch(magnus_ctx* ctx, int64_t h0, int64_t h1, int64_t b
   MG_CUDA(cudaStreamSynchronize(s));
   const int64_t nlist = (int64_t)hc[0], nnz_a = (int64_t)hc[1];
   int rc = MAGNUS_OK;
-  if (nlist > 0 && nnz_a > 0) {
+  // (A nonzeros are numbered in 32 bits, and the segment-position table holds one entry per
+  // (A nonzero, coarse chunk): beyond 4 GB of it the fine-level expand takes the batch)
+  const bool fits = nnz_a < (int64_t(1) << 32) && nnz_a * (int64_t)g.ncc * 4 <= (int64_t(4) << 30);
+  if (nlist > 0 && nnz_a > 0 && fits) {
+    *handled = true;
     ctx->c4_rows += nlist;
     ctx->c4_brows += nnz_a;
     ++ctx->c4_batches;
@@ -1253,9 +1258,10 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
       plan_batch(b + 1, ctx->aux);
       MG_CUDA(cudaEventRecord(ctx->ev_pl[qn], ctx->aux));
     }
+    bool coarse_done = false;
     if (ctx->coarse_dev) {
       int rc4 = coarse_level_batch(ctx, cuts[b], cuts[b + 1], hb[b], hb[b + 1] - hb[b], static_cast<uint16_t*>(bcol[q]),
-                                   static_cast<double*>(bval[q]));
+                                   static_cast<double*>(bval[q]), &coarse_done);
       if (rc4) return rc4;
     }
     ctx->begin(MAGNUS_K_BIN_EXPAND);
@@ -1263,7 +1269,7 @@ static int launch_binned(magnus_ctx* ctx, const int64_t* c_rp, uint32_t* c_col, 
         ctx->A, ctx->B, ctx->listH, ctx->mn, ctx->mx, ctx->sem.shift_num, ctx->choff, ctx->ce, ctx->hbase, hb[b], units,
         nunit, nwin + 3, std::max<int64_t>(max_ent, 1), static_cast<uint16_t*>(bcol[q]), static_cast<double*>(bval[q]),
         ctx->bslot, ctx->bidx, ctx->dir_nwin1, ctx->dir_wlog, e2scr, e2_stride, ctx->err,
-        ctx->coarse_dev ? ctx->cat : nullptr);
+        coarse_done ? ctx->cat : nullptr);
     ctx->end();
     MG_CUDA(cudaEventRecord(ctx->ev_e[q], s));
     // the big-chunk and small-chunk reducers of this batch run on their own streams
