@@ -389,3 +389,20 @@ def test_device_coarse_level(case, sysname, monkeypatch):
     assert_same(spgemm_magnus(A, B, sys=sysp), ref)
     monkeypatch.setenv("MAGNUS_COARSE_PATH", "fine")
     assert_same(spgemm_magnus(A, B, sys=sysp), ref)
+
+
+@pytest.mark.parametrize("knob", ["MAGNUS_SERIAL=0", "MAGNUS_LIGHT_SIDE=0", "MAGNUS_FUSED_ROWS=0",
+                                  "MAGNUS_HEAVY_SYMBOLIC=window", "MAGNUS_BATCH_FRAC=0.05"])
+def test_device_path_knobs_do_not_change_results(knob, monkeypatch):
+    """The tuning knobs of the device path (pipelined reducers on side streams, light rows on
+    the main stream, unfused warp rows, the windowed heavy symbolic kernel, a small reorder buffer) only change
+    the execution strategy: the reference's bits come out under each of them, also with many heavy-row batches."""
+    name, value = knob.split("=")
+    A = generate.rmat(14, 16, seed=31)
+    ref = oracle.spgemm(A, A, B200)
+    monkeypatch.setenv(name, value)
+    assert_same(spgemm_magnus(A, A, sys=B200), ref)
+    monkeypatch.setenv("MAGNUS_BATCH_ELEMS", "150000")
+    assert_same(spgemm_magnus(A, A, sys=B200), ref)
+    H = _hub_matrix()
+    assert_same(spgemm_magnus(H, H, sys=FINE4K), oracle.spgemm(H, H, FINE4K))
