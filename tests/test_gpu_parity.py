@@ -406,3 +406,31 @@ def test_device_path_knobs_do_not_change_results(knob, monkeypatch):
     assert_same(spgemm_magnus(A, A, sys=B200), ref)
     H = _hub_matrix()
     assert_same(spgemm_magnus(H, H, sys=FINE4K), oracle.spgemm(H, H, FINE4K))
+
+
+def _wide_matrix(n_rows, n_cols_b, per_row, seed):
+    rng = np.random.default_rng(seed)
+    cols = np.sort(rng.choice(np.arange(0, n_cols_b, max(1, n_cols_b // 50000), dtype=np.int64), size=(n_rows, per_row)), axis=1)
+    for r in range(n_rows):   # distinct, ascending per row
+        while np.unique(cols[r]).size < per_row:
+            cols[r] = np.sort(rng.choice(np.arange(0, n_cols_b, max(1, n_cols_b // 50000), dtype=np.int64), size=per_row))
+    rp = np.arange(n_rows + 1, dtype=np.int64) * per_row
+    val = generate.uniform_pm1(seed, 0xCD, np.arange(n_rows * per_row, dtype=np.uint64))
+    return CsrMatrix(n_rows, n_cols_b, rp, cols.reshape(-1).astype(np.uint32), val)
+
+
+@pytest.mark.parametrize("n_cols", [(1 << 32) - 3, (1 << 31) + 11, 1 << 26])
+def test_wide_column_space(n_cols):
+    """Columns up to 2^32 - 4 (uint32 indices with the top bit set): light rows with 64-bit sort keys and a heavy
+    row (2000 nonzeros of A) on whichever heavy path the plan allows -- the reference's bits."""
+    rng = np.random.default_rng(5)
+    nk = 2000
+    B = _wide_matrix(nk, n_cols, 12, seed=11)
+    rows = [np.sort(rng.choice(nk, size=(nk if i == 0 else 5), replace=False)) for i in range(64)]
+    rp = np.zeros(65, np.int64)
+    np.cumsum([len(r) for r in rows], out=rp[1:])
+    col = np.concatenate(rows).astype(np.int32)
+    A = CsrMatrix(64, nk, rp, col, generate.uniform_pm1(3, 0xEE, np.arange(col.size, dtype=np.uint64)))
+    for sysp in (B200, HOST2M):
+        ref = oracle.spgemm(A, B, sysp)
+        assert_same(spgemm_magnus(A, B, sys=sysp), ref)
