@@ -434,3 +434,36 @@ def test_wide_column_space(n_cols):
     for sysp in (B200, HOST2M):
         ref = oracle.spgemm(A, B, sysp)
         assert_same(spgemm_magnus(A, B, sys=sysp), ref)
+
+
+@pytest.mark.parametrize("sysname", ["b200", "fine4k", "coarse"])
+def test_signed_zeros_and_cancellation(sysname):
+    """Cancellation (pairs of identical B rows with opposite A coefficients: every sum is zero or a rounding residue
+    that depends on the association), explicit +0.0 / -0.0 values in A and B: the structural entries stay, and every
+    residue and the sign of every zero are the reference's -- on warp, CTA and heavy rows."""
+    rng = np.random.default_rng(17)
+    n, nk = 96, 1500
+    base = generate.uniform_rows(nk // 2, 1 << 15, 24, seed=9)
+    # B: every row twice (k and k + nk/2 are identical), a tenth of the values +-0.0
+    rpb = np.concatenate([np.asarray(base.row_ptr), np.asarray(base.row_ptr)[1:] + int(base.row_ptr[-1])])
+    colb = np.concatenate([np.asarray(base.col), np.asarray(base.col)])
+    valb = np.concatenate([np.asarray(base.val), np.asarray(base.val)]).copy()
+    z = rng.random(valb.size) < 0.1
+    valb[z] = np.where(rng.random(int(z.sum())) < 0.5, 0.0, -0.0)
+    valb[valb.size // 2:] = valb[:valb.size // 2]
+    B = CsrMatrix(nk, 1 << 15, rpb.astype(np.int64), colb.astype(np.int32), valb)
+    rows, vals = [], []
+    for i in range(n):
+        m = (700, 60, 8)[i % 3] if i else 740   # heavy, CTA and warp rows
+        ks = np.sort(rng.choice(nk // 2, size=m, replace=False))
+        a = generate.uniform_pm1(i + 1, 0xAA, np.arange(m, dtype=np.uint64))
+        a[rng.random(m) < 0.05] = -0.0
+        rows.append(np.concatenate([ks, ks + nk // 2]))      # k and its twin ...
+        vals.append(np.concatenate([a, -a]))                 # ... with opposite coefficients
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum([len(r) for r in rows], out=rp[1:])
+    A = CsrMatrix(n, nk, rp, np.concatenate(rows).astype(np.int32), np.concatenate(vals))
+    sysp = {"b200": B200, "fine4k": FINE4K, "coarse": COARSE}[sysname]
+    ref = oracle.spgemm(A, B, sysp)
+    assert ref.val.size and np.mean(np.abs(ref.val) < 1e-12) > 0.99   # (near-)exact cancellation everywhere
+    assert_same(spgemm_magnus(A, B, sys=sysp), ref)
